@@ -1,0 +1,532 @@
+// C ABI of the B200 GADI hot path (include/gadi_b200.h): context lifetime,
+// host <-> device transfers in the reference's layout, the ||A||_2 power
+// iteration, and the outer step that chains H-solve, S-solve and the fused
+// update/residual/monitor pass.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include "engine.cuh"
+
+namespace gadi {
+
+static thread_local std::string g_err;
+int set_error(const std::string& msg, int code) {
+  g_err = msg;
+  return code;
+}
+
+static size_t fmt_bytes(int f) {
+  switch (f) {
+    case GADI_BF16:
+    case GADI_FP16: return 2;
+    case GADI_FP32: return 4;
+    default: return 8;
+  }
+}
+
+static EngineVT* engine_for(int us) {
+  switch (us) {
+    case GADI_BF16: return &engine_bf16;
+    case GADI_FP16: return &engine_fp16;
+    case GADI_FP32: return &engine_fp32;
+    case GADI_FP64: return &engine_fp64;
+    default: return nullptr;
+  }
+}
+
+static int grid_blocks_pw(const Ctx* c) { return std::max(1, c->sms * 16); }
+
+static int launch_1d(const Ctx* c, long long n) {
+  return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)c->sms * 16));
+}
+
+// host block layout -> device internal layout (crd: interleaved)
+static int upload(Ctx* c, const double* host, double* dev) {
+  if (c->kind == GADI_COMPLEX) {
+    GADI_CUDA(cudaMemcpyAsync(c->tmp, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+    interleave_kernel<<<launch_1d(c, c->n / 2), 256, 0, c->stream>>>(c->tmp, dev, c->n / 2);
+    c->launches++;
+  } else {
+    GADI_CUDA(cudaMemcpyAsync(dev, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+  }
+  GADI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+static int download(Ctx* c, const double* dev, double* host) {
+  if (c->kind == GADI_COMPLEX) {
+    deinterleave_kernel<<<launch_1d(c, c->n / 2), 256, 0, c->stream>>>(dev, c->tmp, c->n / 2);
+    c->launches++;
+    GADI_CUDA(cudaMemcpyAsync(host, c->tmp, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    GADI_CUDA(cudaMemcpyAsync(host, dev, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+  }
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+template <int DIM, int ZS, bool CPLX, bool TRANS>
+static int norm_pass(Ctx* c, const double* in, double* out) {
+  typedef GeoT<double, DIM, ZS> G;
+  NormPass<G, CPLX, TRANS> p;
+  p.ns = c->nst;
+  p.in = in;
+  p.outv = out;
+  p.v = c->v64;
+  p.A = TRANS ? c->AT : c->A;
+  return launch_sweep(c, p);
+}
+
+template <bool TRANS>
+static int norm_pass_d(Ctx* c, const double* in, double* out) {
+  if (c->kind == GADI_COMPLEX) return norm_pass<2, 2, true, TRANS>(c, in, out);
+  if (c->ndim == 3) return norm_pass<3, 1, false, TRANS>(c, in, out);
+  return norm_pass<2, 1, false, TRANS>(c, in, out);
+}
+
+// Vectors carry guard bands so the TMA sweep may copy whole padded rows
+// (16 bytes before the first and up to a tile past the last element).
+static constexpr size_t GUARD = 256 * 1024;
+static cudaError_t guarded_malloc(void** p, size_t bytes) {
+  unsigned char* raw = nullptr;
+  cudaError_t e = cudaMalloc((void**)&raw, bytes + 2 * GUARD);
+  if (e != cudaSuccess) return e;
+  *p = raw + GUARD;
+  return cudaMemset(raw, 0, GUARD) == cudaSuccess && cudaMemset(raw + GUARD + bytes, 0, GUARD) == cudaSuccess
+             ? cudaSuccess
+             : cudaErrorUnknown;
+}
+static void guarded_free(void* p) {
+  if (p) cudaFree(reinterpret_cast<unsigned char*>(p) - GUARD);
+}
+
+static void free_ctx(Ctx* c) {
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* gp[] = {c->b, c->x[0], c->x[1], c->r, c->xs, c->tmp, c->R, c->P[0], c->P[1], c->Z, c->RB, c->Y};
+  for (void* p : gp) guarded_free(p);
+  void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst};
+  for (void* p : sp)
+    if (p) cudaFree(p);
+  void* hp[] = {c->h_hst, c->h_sst, c->h_osum, c->h_nst};
+  for (void* p : hp)
+    if (p) cudaFreeHost(p);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+}  // namespace gadi
+
+using namespace gadi;
+
+#define ALLOCG(ptr, bytes)                                                                     \
+  do {                                                                                         \
+    cudaError_t e_ = guarded_malloc((void**)&(ptr), (bytes));                                  \
+    if (e_ != cudaSuccess) {                                                                   \
+      free_ctx(c);                                                                             \
+      delete h;                                                                                \
+      return set_error(std::string("cudaMalloc ") + #ptr + ": " + cudaGetErrorString(e_),   \
+                       e_ == cudaErrorMemoryAllocation ? GADI_ERR_OOM : GADI_ERR_CUDA);        \
+    }                                                                                          \
+  } while (0)
+
+#define ALLOC(ptr, bytes)                                                                      \
+  do {                                                                                         \
+    cudaError_t e_ = cudaMalloc((void**)&(ptr), (bytes));                                      \
+    if (e_ != cudaSuccess) {                                                                   \
+      free_ctx(c);                                                                             \
+      delete h;                                                                                \
+      return set_error(std::string("cudaMalloc ") + #ptr + ": " + cudaGetErrorString(e_),   \
+                       e_ == cudaErrorMemoryAllocation ? GADI_ERR_OOM : GADI_ERR_CUDA);        \
+    }                                                                                          \
+  } while (0)
+
+extern "C" {
+
+const char* gadi_last_error(void) { return g_err.c_str(); }
+
+const char* gadi_build_info(void) {
+  return "gadi_b200: sm_100a matrix-free GADI kernels (2.5-D stencil sweeps, device-side Krylov scalars)";
+}
+
+int gadi_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return set_error(std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e), GADI_ERR_CUDA);
+  }
+  *count = n;
+  return 0;
+}
+
+int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out) {
+  if (!desc || !out) return set_error("null argument", GADI_ERR_ARG);
+  *out = nullptr;
+  if (desc->kind == GADI_CSR) return set_error("CSR operators are handled by the CSR engine", GADI_ERR_UNSUPPORTED);
+  if (desc->kind != GADI_STENCIL && desc->kind != GADI_COMPLEX) return set_error("unknown kind", GADI_ERR_ARG);
+  EngineVT* vt = engine_for(desc->u_s);
+  if (!vt) return set_error("u_s must be bf16, fp16, fp32 or fp64", GADI_ERR_ARG);
+  gadi_ctx* h = new gadi_ctx();
+  Ctx* c = &h->c;
+  c->d = *desc;
+  c->d.v = nullptr;
+  c->device = device;
+  c->kind = desc->kind;
+  c->ndim = desc->ndim;
+  c->us = desc->u_s;
+  c->u = desc->u;
+  c->ur = desc->u_r;
+  c->ssz = fmt_bytes(desc->u_s);
+  c->vt = vt;
+  c->no_tma = getenv("GADI_NO_TMA") ? atoi(getenv("GADI_NO_TMA")) : 0;
+  if (getenv("GADI_WAVES")) c->waves = std::max(1, atoi(getenv("GADI_WAVES")));
+  if (getenv("GADI_MIN_CHUNK")) c->min_chunk = std::max(1, atoi(getenv("GADI_MIN_CHUNK")));
+  if (c->kind == GADI_STENCIL) {
+    c->nx = (int)desc->dims[0];
+    c->ny = (int)desc->dims[1];
+    c->nz = (int)desc->dims[2];
+    if (c->ndim == 2 && c->ny != 1) {
+      delete h;
+      return set_error("2-D stencils use dims (n_g, 1, n_g)", GADI_ERR_ARG);
+    }
+  } else {
+    c->nx = (int)desc->dims[0];
+    c->ny = 1;
+    c->nz = 2 * (int)desc->dims[2];
+    c->ndim = 2;
+    if (c->ur != GADI_FP64) {
+      delete h;
+      return set_error("complex family supports u_r = fp64 only", GADI_ERR_UNSUPPORTED);
+    }
+  }
+  c->n = (long long)c->nx * c->ny * c->nz;
+  if (c->n != desc->n || c->n <= 0) {
+    delete h;
+    return set_error("dims do not match n", GADI_ERR_ARG);
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete h;
+    return set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e), GADI_ERR_CUDA);
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) c->sms = prop.multiProcessorCount;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete h;
+    return set_error(std::string("cudaStreamCreate: ") + cudaGetErrorString(e), GADI_ERR_CUDA);
+  }
+  // coefficients
+  c->A = coef_of(desc->A);
+  c->AT = transpose_coef(c->A);
+  c->H = coef_of(desc->H);
+  c->S = coef_of(desc->S);
+  c->ST = transpose_coef(c->S);
+  c->A32 = cast_coef<float>(c->A);
+  // partials stride: the largest grid any pass of this context launches
+  {
+    int mx = grid_blocks_pw(c) + 64;
+    const int vzs = std::max(2, (int)(16 / c->ssz));
+    const int bz = c->ndim == 3 ? 32 : 64, by = c->ndim == 3 ? 8 : 1;
+    const int tzs[2] = {bz * vzs, bz * 2};
+    for (int t : tzs) {
+      c->pstride = 0;
+      SweepGeom g = make_geom(c, t, by, 1);
+      mx = std::max(mx, geom_blocks(g));
+    }
+    mx = std::max(mx, c->sms * 16 * c->waves + 64);
+    c->pstride = mx;
+  }
+  const size_t n8 = sizeof(double) * (size_t)c->n, ns = c->ssz * (size_t)c->n;
+  ALLOCG(c->b, n8);
+  ALLOCG(c->x[0], n8);
+  ALLOCG(c->x[1], n8);
+  ALLOCG(c->r, n8);
+  ALLOCG(c->tmp, n8);
+  ALLOCG(c->R, ns);
+  ALLOCG(c->P[0], ns);
+  ALLOCG(c->P[1], ns);
+  ALLOCG(c->Z, ns);
+  ALLOCG(c->RB, ns);
+  ALLOCG(c->Y, ns);
+  ALLOC(c->partials, sizeof(double) * 8 * (size_t)c->pstride);
+  ALLOC(c->ticket, sizeof(unsigned int));
+  ALLOC(c->hst, sizeof(InnerState));
+  ALLOC(c->sst, sizeof(InnerState));
+  ALLOC(c->osum, sizeof(OuterSums));
+  ALLOC(c->nst, sizeof(NormState));
+  if (c->kind == GADI_COMPLEX) {
+    if (!desc->v) {
+      free_ctx(c);
+      delete h;
+      return set_error("complex family needs v", GADI_ERR_ARG);
+    }
+    ALLOC(c->v64, sizeof(double) * (size_t)(c->n / 2));
+    ALLOC(c->VS, c->ssz * (size_t)(c->n / 2));
+  }
+#define CHK(call)                                                                    \
+  do {                                                                               \
+    cudaError_t e2_ = (call);                                                        \
+    if (e2_ != cudaSuccess) {                                                        \
+      free_ctx(c);                                                                   \
+      delete h;                                                                      \
+      return set_error(std::string(#call) + ": " + cudaGetErrorString(e2_), GADI_ERR_CUDA); \
+    }                                                                                \
+  } while (0)
+  CHK(cudaMallocHost((void**)&c->h_hst, sizeof(InnerState)));
+  CHK(cudaMallocHost((void**)&c->h_sst, sizeof(InnerState)));
+  CHK(cudaMallocHost((void**)&c->h_osum, sizeof(OuterSums)));
+  CHK(cudaMallocHost((void**)&c->h_nst, sizeof(NormState)));
+  for (auto& ev : c->ev) CHK(cudaEventCreate(&ev));
+  CHK(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream));
+  CHK(cudaMemsetAsync(c->hst, 0, sizeof(InnerState), c->stream));
+  CHK(cudaMemsetAsync(c->sst, 0, sizeof(InnerState), c->stream));
+  CHK(cudaMemsetAsync(c->x[0], 0, n8, c->stream));
+  CHK(cudaMemsetAsync(c->x[1], 0, n8, c->stream));
+  CHK(cudaMemsetAsync(c->Y, 0, ns, c->stream));
+  if (c->kind == GADI_COMPLEX) {
+    CHK(cudaMemcpyAsync(c->v64, desc->v, sizeof(double) * (size_t)(c->n / 2), cudaMemcpyHostToDevice, c->stream));
+    int rc = c->vt->quantize(c, c->v64, c->VS, c->n / 2);
+    if (rc) {
+      free_ctx(c);
+      delete h;
+      return rc;
+    }
+  }
+  CHK(cudaStreamSynchronize(c->stream));
+#undef CHK
+  *out = h;
+  return 0;
+}
+
+int gadi_ctx_destroy(gadi_ctx* h) {
+  if (!h) return 0;
+  free_ctx(&h->c);
+  delete h;
+  return 0;
+}
+
+int gadi_set_rhs(gadi_ctx* h, const double* b) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  GADI_TRY(upload(c, b, c->b));
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int gadi_gen_rhs_ones(gadi_ctx* h) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  RhsOnes p;
+  p.nx = c->nx;
+  p.ny = c->ny;
+  p.nz = c->nz;
+  p.zs = c->kind == GADI_COMPLEX ? 2 : 1;
+  p.plane = (long long)c->ny * c->nz;
+  p.A = c->A;
+  p.v = c->v64;
+  p.b = c->b;
+  rhs_ones_kernel<<<launch_1d(c, c->n), 256, 0, c->stream>>>(p, c->n);
+  c->launches++;
+  GADI_CUDA(cudaGetLastError());
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int gadi_get_rhs(gadi_ctx* h, double* b) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  return download(c, c->b, b);
+}
+
+int gadi_set_exact(gadi_ctx* h, const double* xs, int all_ones) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  if (xs) {
+    if (!c->xs) GADI_CUDA(guarded_malloc((void**)&c->xs, sizeof(double) * (size_t)c->n));
+    GADI_TRY(upload(c, xs, c->xs));
+    GADI_CUDA(cudaStreamSynchronize(c->stream));
+    c->has_exact = 1;
+    c->ones = 0;
+  } else {
+    c->has_exact = all_ones ? 1 : 0;
+    c->ones = all_ones ? 1 : 0;
+  }
+  return 0;
+}
+
+int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int maxit, double* sigma, int* iterations) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  double* w = c->x[0];
+  double* t = c->x[1];
+  GADI_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  if (v0) {
+    GADI_TRY(upload(c, v0, w));
+  } else {
+    const int nb = launch_1d(c, c->n);
+    randn_kernel<<<nb, 256, 0, c->stream>>>(w, c->n, (unsigned long long)seed);
+    sumsq_kernel<<<nb, 256, 0, c->stream>>>(w, c->n, c->partials);
+    scale_by_norm_kernel<<<nb, 256, 0, c->stream>>>(w, c->n, c->partials, nb);
+    c->launches += 3;
+    GADI_CUDA(cudaGetLastError());
+  }
+  norm_state_init<<<1, 1, 0, c->stream>>>(c->nst, tol, maxit);
+  c->launches++;
+  int launched = 0, batch = 64;
+  bool polled = false;
+  while (launched < maxit) {
+    const int nb = std::min(batch, maxit - launched);
+    for (int j = 0; j < nb; ++j) {
+      GADI_TRY(norm_pass_d<false>(c, w, t));
+      GADI_TRY(norm_pass_d<true>(c, t, w));
+    }
+    launched += nb;
+    GADI_CUDA(cudaMemcpyAsync(c->h_nst, c->nst, sizeof(NormState), cudaMemcpyDeviceToHost, c->stream));
+    GADI_CUDA(cudaStreamSynchronize(c->stream));
+    polled = true;
+    if (c->h_nst->done) break;
+    batch = 128;
+  }
+  if (!polled) {
+    GADI_CUDA(cudaMemcpyAsync(c->h_nst, c->nst, sizeof(NormState), cudaMemcpyDeviceToHost, c->stream));
+    GADI_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  GADI_CUDA(cudaEventRecord(c->ev[5], c->stream));
+  GADI_CUDA(cudaEventSynchronize(c->ev[5]));
+  float ms = 0.f;
+  GADI_CUDA(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]));
+  c->last_norm_ms = ms;
+  *sigma = c->h_nst->sigma;
+  if (iterations) *iterations = c->h_nst->it;
+  // leave x = 0 for the solve
+  GADI_CUDA(cudaMemsetAsync(c->x[0], 0, sizeof(double) * (size_t)c->n, c->stream));
+  GADI_CUDA(cudaMemsetAsync(c->x[1], 0, sizeof(double) * (size_t)c->n, c->stream));
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+static void fill_scalars(const OuterSums* s, gadi_outer_scalars* o) {
+  o->sum_r2 = s->v[0];
+  o->max_r = s->v[1];
+  o->sum_ralg2 = s->v[2];
+  o->sum_x2 = s->v[3];
+  o->sum_e2 = s->v[4];
+  o->sum_ae2 = s->v[5];
+}
+
+static void fill_stats(const InnerState* s, gadi_inner_stats* o) {
+  o->iterations = s->it;
+  o->converged = s->converged;
+  o->breakdown = s->breakdown;
+  o->pad = 0;
+  o->final_relative_residual = s->relres;
+}
+
+int gadi_outer_begin(gadi_ctx* h, gadi_outer_scalars* out) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  GADI_CUDA(cudaMemsetAsync(c->x[c->xcur], 0, sizeof(double) * (size_t)c->n, c->stream));
+  GADI_CUDA(cudaMemsetAsync(c->Y, 0, c->ssz * (size_t)c->n, c->stream));
+  GADI_TRY(c->vt->outer(c, 1.0, c->has_exact));
+  GADI_CUDA(cudaMemcpyAsync(c->h_osum, c->osum, sizeof(OuterSums), cudaMemcpyDeviceToHost, c->stream));
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  if (out) fill_scalars(c->h_osum, out);
+  c->pred_h = 4;
+  c->pred_s = 4;
+  return 0;
+}
+
+int gadi_outer_step(gadi_ctx* h, const gadi_step_args* a, gadi_outer_scalars* out, gadi_inner_stats* hs,
+                    gadi_inner_stats* ss, gadi_phase_times* t) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  GADI_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  GADI_TRY(c->vt->h_solve(c, a->scale, a->inner_tol, a->maxit_h));
+  GADI_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  GADI_TRY(c->vt->s_solve(c, a->coeff, a->inner_tol, a->maxit_s));
+  GADI_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  GADI_TRY(c->vt->outer(c, a->scale, c->has_exact));
+  GADI_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  GADI_CUDA(cudaMemcpyAsync(c->h_osum, c->osum, sizeof(OuterSums), cudaMemcpyDeviceToHost, c->stream));
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  if (out) fill_scalars(c->h_osum, out);
+  if (hs) fill_stats(c->h_hst, hs);
+  if (ss) fill_stats(c->h_sst, ss);
+  if (t) {
+    float m0 = 0.f, m1 = 0.f, m2 = 0.f;
+    GADI_CUDA(cudaEventElapsedTime(&m0, c->ev[0], c->ev[1]));
+    GADI_CUDA(cudaEventElapsedTime(&m1, c->ev[1], c->ev[2]));
+    GADI_CUDA(cudaEventElapsedTime(&m2, c->ev[2], c->ev[3]));
+    t->inner_h = m0;
+    t->inner_s = m1;
+    t->residual = m2;  // fused update + residual + monitor pass
+    t->update = 0.0;
+    t->monitor = 0.0;
+  }
+  return 0;
+}
+
+int gadi_get_x(gadi_ctx* h, double* x) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  return download(c, c->x[c->xcur], x);
+}
+
+int gadi_h_solve(gadi_ctx* h, const double* rhs, double tol, int maxit, double* x, gadi_inner_stats* st) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  GADI_TRY(upload(c, rhs, c->r));
+  c->pred_h = std::min(maxit, 16);
+  GADI_TRY(c->vt->h_solve(c, 1.0, tol, maxit));
+  GADI_TRY(c->vt->widen(c, c->Z, c->x[c->xcur ^ 1], c->n));
+  GADI_TRY(download(c, c->x[c->xcur ^ 1], x));
+  if (st) fill_stats(c->h_hst, st);
+  return 0;
+}
+
+int gadi_s_solve(gadi_ctx* h, const double* rhs, double tol, int maxit, double* x, gadi_inner_stats* st) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  GADI_TRY(upload(c, rhs, c->r));
+  GADI_TRY(c->vt->quantize(c, c->r, c->Z, c->n));
+  c->pred_s = std::min(maxit, 16);
+  GADI_TRY(c->vt->s_solve(c, 1.0, tol, maxit));
+  GADI_TRY(c->vt->widen(c, c->Y, c->x[c->xcur ^ 1], c->n));
+  GADI_TRY(download(c, c->x[c->xcur ^ 1], x));
+  if (st) fill_stats(c->h_sst, st);
+  return 0;
+}
+
+int gadi_spmv(gadi_ctx* h, int op, int strict, const double* x, double* y) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  if (op < 0 || op > 3) return set_error("op must be 0..3", GADI_ERR_ARG);
+  GADI_TRY(upload(c, x, c->r));
+  if (op == 0) {
+    norm_state_init<<<1, 1, 0, c->stream>>>(c->nst, 0.0, 1);
+    c->launches++;
+    GADI_TRY(norm_pass_d<false>(c, c->r, c->x[c->xcur ^ 1]));
+  } else {
+    GADI_TRY(c->vt->apply(c, op, strict, c->r, c->x[c->xcur ^ 1]));
+  }
+  GADI_TRY(download(c, c->x[c->xcur ^ 1], y));
+  return 0;
+}
+
+int gadi_residual(gadi_ctx* h, const double* x, double* r) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  GADI_TRY(upload(c, x, c->x[c->xcur]));
+  GADI_CUDA(cudaMemsetAsync(c->Y, 0, c->ssz * (size_t)c->n, c->stream));
+  GADI_TRY(c->vt->outer(c, 1.0, 0));  // x_new = x + 0 ; r = b - A x
+  return download(c, c->r, r);
+}
+
+double gadi_last_norm_ms(gadi_ctx* h) { return h->c.last_norm_ms; }
+int64_t gadi_kernel_launches(gadi_ctx* h) { return h->c.launches; }
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// Host-side context of one solve: device buffers, stream, device-resident
+// scalar states and their pinned host mirrors.  Shared by the per-precision
+// engines (engine_*.cu) and the C-ABI (api.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <string>
+#include <vector>
+#include "../../include/gadi_b200.h"
+#include "passes.cuh"
+
+namespace gadi {
+
+struct Ctx;
+
+// Per-u_s-precision entry points (one table per storage type).
+struct EngineVT {
+  int (*h_solve)(Ctx*, double scale, double tol, int maxit);  // rhs: c->r (fp64)
+  int (*s_solve)(Ctx*, double coeff, double tol, int maxit);  // rhs: coeff * c->Z
+  int (*outer)(Ctx*, double scale, int has_e);                // x += y/scale ; r ; sums
+  int (*apply)(Ctx*, int op, int strict, const double* xdev, double* ydev);
+  int (*quantize)(Ctx*, const double* in, void* out, long long n);
+  int (*widen)(Ctx*, const void* in, double* out, long long n);
+};
+
+struct Ctx {
+  gadi_problem_desc d;  // copy (host pointers are not retained)
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int kind = 0, ndim = 2;
+  int nx = 1, ny = 1, nz = 1;  // device grid (complex: nz = 2 n_g)
+  long long n = 0;
+  int us = GADI_FP64, u = GADI_FP64, ur = GADI_FP64;
+  size_t ssz = 8;  // bytes per u_s element
+  int sms = 148;
+
+  // fp64 vectors
+  double* b = nullptr;
+  double* x[2] = {nullptr, nullptr};
+  int xcur = 0;
+  double* r = nullptr;
+  double* xs = nullptr;
+  double* v64 = nullptr;  // crd potential
+  double* tmp = nullptr;  // staging for host<->device permutations
+  // u_s vectors (typed by the engine)
+  void* R = nullptr;
+  void* P[2] = {nullptr, nullptr};
+  void* Z = nullptr;
+  void* RB = nullptr;
+  void* Y = nullptr;
+  void* VS = nullptr;  // crd potential in u_s
+
+  double* partials = nullptr;
+  int pstride = 0;
+  unsigned int* ticket = nullptr;
+  InnerState* hst = nullptr;
+  InnerState* sst = nullptr;
+  OuterSums* osum = nullptr;
+  NormState* nst = nullptr;
+  // pinned mirrors
+  InnerState* h_hst = nullptr;
+  InnerState* h_sst = nullptr;
+  OuterSums* h_osum = nullptr;
+  NormState* h_nst = nullptr;
+
+  cudaEvent_t ev[6] = {};
+  int has_exact = 0, ones = 0;
+  int pred_h = 4, pred_s = 4;  // iteration-count predictions for launch batching
+  long long launches = 0;
+  int no_tma = 0;  // force the register-prefetch sweep (testing)
+  int waves = 1;      // grid size in waves of resident CTAs (TMA sweep)
+  int min_chunk = 8;  // lower bound on planes per CTA
+  double last_norm_ms = 0.0;
+
+  CoefT<double> A, AT, H, S, ST;
+  CoefT<float> A32;
+  EngineVT* vt = nullptr;
+};
+
+int set_error(const std::string& msg, int code);
+
+#define GADI_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return ::gadi::set_error(std::string(#call) + ": " + cudaGetErrorString(e_), GADI_ERR_CUDA); \
+  } while (0)
+
+inline CoefT<double> coef_of(const gadi_coef& c) {
+  CoefT<double> o;
+  o.d = c.d;
+  for (int i = 0; i < 3; ++i) {
+    o.lo[i] = c.lo[i];
+    o.up[i] = c.up[i];
+  }
+  return o;
+}
+inline CoefT<double> transpose_coef(const CoefT<double>& c) {
+  CoefT<double> o = c;
+  for (int i = 0; i < 3; ++i) {
+    o.lo[i] = c.up[i];
+    o.up[i] = c.lo[i];
+  }
+  return o;
+}
+template <class CT>
+inline CoefT<CT> cast_coef(const CoefT<double>& c) {
+  CoefT<CT> o;
+  o.d = (CT)c.d;
+  for (int i = 0; i < 3; ++i) {
+    o.lo[i] = (CT)c.lo[i];
+    o.up[i] = (CT)c.up[i];
+  }
+  return o;
+}
+
+// Sweep geometry for a pass with tile TZ x TY.  `slots` = CTAs resident on
+// the whole GPU (occupancy x SMs): the x-chunks are sized so the grid is
+// about `waves` full waves (long chunks amortise the pipeline fill and the
+// two overlap planes of every chunk); 0 keeps the legacy target.
+inline SweepGeom make_geom(const Ctx* c, int TZ, int TY, int VZ, long long slots = 0) {
+  SweepGeom g;
+  g.nx = c->nx;
+  g.ny = c->ny;
+  g.nz = c->nz;
+  g.plane = (long long)c->ny * c->nz;
+  g.nzt = (c->nz + TZ - 1) / TZ;
+  g.nyt = (c->ny + TY - 1) / TY;
+  const long long tiles = (long long)g.nzt * g.nyt;
+  long long xc;
+  if (slots > 0) {
+    const long long want = slots * (long long)c->waves;
+    const long long chunks = std::max(1LL, want / tiles);
+    xc = (c->nx + chunks - 1) / chunks;
+    xc = std::max(xc, std::min<long long>(c->nx, c->min_chunk));
+  } else {
+    const long long target = (long long)c->sms * 12;
+    xc = (c->nx * tiles + target - 1) / target;
+  }
+  if (xc < 1) xc = 1;
+  if (xc > c->nx) xc = c->nx;
+  g.xchunk = (int)xc;
+  g.pstride = c->pstride;
+  g.vec = (c->nz % VZ) == 0 ? 1 : 0;
+  return g;
+}
+inline int geom_blocks(const SweepGeom& g) {
+  return g.nzt * g.nyt * ((g.nx + g.xchunk - 1) / g.xchunk);
+}
+
+extern EngineVT engine_bf16, engine_fp16, engine_fp32, engine_fp64;
+
+}  // namespace gadi
+
+struct gadi_ctx {
+  gadi::Ctx c;
+};

@@ -1,0 +1,348 @@
+// Per-u_s-precision engine: launches the fused passes of the inner solves and
+// of the outer step for one storage type ST, dispatching on the operator
+// family (2-D / 3-D real stencil, crd complex).  Instantiated once per ST in
+// engine_<st>.cu so the precisions compile in parallel.
+//
+// Inner Krylov loops run device-driven: every pass reads the solve state
+// (alpha, beta, it, done) from device memory and the last CTA of each pass
+// writes the next scalars, so the host only enqueues.  Kernels launched after
+// convergence exit at their first instruction.  The host enqueues a predicted
+// number of iterations (the count of the previous outer step), then polls the
+// `done` flag once per batch.
+#pragma once
+#include <algorithm>
+#include "ctx.h"
+#include "pointwise.cuh"
+
+namespace gadi {
+
+// True when every input row of pass P starts 16-byte aligned (TMA path).
+template <class P>
+inline bool tma_aligned(const Ctx* c) {
+  if (!P::TMA_OK || c->no_tma) return false;
+  for (int j = 0; j < P::NIN; ++j)
+    if (((long long)c->nz * P::in_esz(j)) % 16) return false;
+  for (int j = 0; j < P::NE; ++j)
+    if (((long long)c->nz * P::epi_esz(j)) % 16) return false;
+  return (c->nz % P::VZ) == 0;
+}
+
+template <class P>
+inline int launch_sweep(Ctx* c, P& p) {
+  using S = SweepShape<P>;
+  p.partials = c->partials;
+  p.ticket = c->ticket;
+  if (tma_aligned<P>(c)) {
+    const size_t smem = TmaShape<P>::SMEM;
+    static int occ = 0;
+    if (!occ) {
+      GADI_CUDA(cudaFuncSetAttribute(sweep_tma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma_kernel<P>, P::NT + 32, smem));
+      if (occ < 1) occ = 1;
+    }
+    p.g = make_geom(c, S::TZ, S::TY, P::VZ, (long long)occ * c->sms);
+    const int nb = geom_blocks(p.g);
+    if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
+    sweep_tma_kernel<P><<<nb, P::NT + 32, smem, c->stream>>>(p);
+  } else {
+    p.g = make_geom(c, S::TZ, S::TY, P::VZ);
+    const int nb = geom_blocks(p.g);
+    if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
+    const size_t smem = S::SMEM;
+    if (smem > 48 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        GADI_CUDA(cudaFuncSetAttribute(sweep_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+      }
+    }
+    sweep_kernel<P><<<nb, P::NT, smem, c->stream>>>(p);
+  }
+  c->launches++;
+  GADI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <class P>
+inline int launch_pw(Ctx* c, P& p) {
+  p.n = c->n;
+  p.partials = c->partials;
+  p.ticket = c->ticket;
+  p.pstride = c->pstride;
+  const long long chunks = (c->n + (long long)PW_NT * P::VZ - 1) / ((long long)PW_NT * P::VZ);
+  int nb = (int)std::min<long long>(chunks, (long long)c->sms * 8);
+  nb = std::max(nb, 1);
+  pointwise_kernel<P><<<nb, PW_NT, 0, c->stream>>>(p);
+  c->launches++;
+  GADI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+#define GADI_TRY(x)          \
+  do {                       \
+    int rc_ = (x);           \
+    if (rc_) return rc_;     \
+  } while (0)
+
+// Poll the device state of an inner solve.
+inline int poll_state(Ctx* c, InnerState* dev, InnerState* host) {
+  GADI_CUDA(cudaMemcpyAsync(host, dev, sizeof(InnerState), cudaMemcpyDeviceToHost, c->stream));
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+template <class ST>
+struct Engine {
+  typedef typename CTOf<ST>::type CT;
+
+  // ------------------------------------------------------------ H-solve (CG)
+  template <int DIM, int ZS>
+  static int h_solve_t(Ctx* c, double scale, double tol, int maxit) {
+    typedef GeoT<ST, DIM, ZS> G;
+    HcgInit<ST> hi;
+    hi.r64 = c->r;
+    hi.rs = (ST*)c->R;
+    hi.z = (ST*)c->Z;
+    hi.st = c->hst;
+    hi.scale = scale;
+    hi.tol = tol;
+    hi.maxit = maxit;
+    GADI_TRY(launch_pw(c, hi));
+    const CoefT<CT> H = cast_coef<CT>(c->H);
+    ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
+    int launched = 0;
+    int batch = std::max(1, c->pred_h + 1);
+    bool polled = false;
+    while (launched < maxit) {
+      const int nb = std::min(batch, maxit - launched);
+      for (int j = 0; j < nb; ++j) {
+        const int k = launched + j;
+        HcgA<G> a;
+        a.st = c->hst;
+        a.r = (const ST*)c->R;
+        a.pin = P[k & 1];
+        a.pout = P[(k + 1) & 1];
+        a.H = H;
+        GADI_TRY(launch_sweep(c, a));
+        HcgB<G> b;
+        b.st = c->hst;
+        b.p = P[(k + 1) & 1];
+        b.z = (ST*)c->Z;
+        b.r = (ST*)c->R;
+        b.H = H;
+        GADI_TRY(launch_sweep(c, b));
+      }
+      launched += nb;
+      GADI_TRY(poll_state(c, c->hst, c->h_hst));
+      polled = true;
+      if (c->h_hst->done) break;
+      batch = std::max(2, c->pred_h / 4 + 1);
+    }
+    if (!polled) GADI_TRY(poll_state(c, c->hst, c->h_hst));
+    c->pred_h = c->h_hst->it;
+    return 0;
+  }
+
+  // ------------------------------------------------------------ S-solve (CGNR)
+  template <int DIM>
+  static int s_solve_real(Ctx* c, double coeff, double tol, int maxit) {
+    typedef GeoT<ST, DIM, 1> G;
+    const CoefT<CT> S = cast_coef<CT>(c->S), STc = cast_coef<CT>(c->ST);
+    CgnrInit<G> ci;
+    ci.st = c->sst;
+    ci.z = (const ST*)c->Z;
+    ci.r = (ST*)c->R;
+    ci.rbar = (ST*)c->RB;
+    ci.y = (ST*)c->Y;
+    ci.ST_ = STc;
+    ci.coeff = (CT)coeff;
+    ci.tol = tol;
+    ci.maxit = maxit;
+    GADI_TRY(launch_sweep(c, ci));
+    ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
+    int launched = 0;
+    int batch = std::max(1, c->pred_s + 1);
+    bool polled = false;
+    while (launched < maxit) {
+      const int nb = std::min(batch, maxit - launched);
+      for (int j = 0; j < nb; ++j) {
+        const int k = launched + j;
+        CgnrP1<G> p1;
+        p1.st = c->sst;
+        p1.rbar = (const ST*)c->RB;
+        p1.pin = P[k & 1];
+        p1.pout = P[(k + 1) & 1];
+        p1.S = S;
+        GADI_TRY(launch_sweep(c, p1));
+        CgnrP2<G> p2;
+        p2.st = c->sst;
+        p2.p = P[(k + 1) & 1];
+        p2.y = (ST*)c->Y;
+        p2.r = (ST*)c->R;
+        p2.S = S;
+        GADI_TRY(launch_sweep(c, p2));
+        CgnrP3<G> p3;
+        p3.st = c->sst;
+        p3.r = (const ST*)c->R;
+        p3.rbar = (ST*)c->RB;
+        p3.ST_ = STc;
+        GADI_TRY(launch_sweep(c, p3));
+      }
+      launched += nb;
+      GADI_TRY(poll_state(c, c->sst, c->h_sst));
+      polled = true;
+      if (c->h_sst->done) break;
+      batch = std::max(2, c->pred_s / 4 + 1);
+    }
+    if (!polled) GADI_TRY(poll_state(c, c->sst, c->h_sst));
+    c->pred_s = c->h_sst->it;
+    return 0;
+  }
+
+  static int s_solve_cplx(Ctx* c, double coeff, double tol, int maxit) {
+    const CT al = (CT)c->d.alpha_s;
+    CInit<ST> ci;
+    ci.vs = (const ST*)c->VS;
+    ci.al = al;
+    ci.z = (const ST*)c->Z;
+    ci.r = (ST*)c->R;
+    ci.y = (ST*)c->Y;
+    ci.st = c->sst;
+    ci.coeff = (CT)coeff;
+    ci.tol = tol;
+    ci.maxit = maxit;
+    GADI_TRY(launch_pw(c, ci));
+    int launched = 0;
+    int batch = std::max(1, c->pred_s + 1);
+    bool polled = false;
+    while (launched < maxit) {
+      const int nb = std::min(batch, maxit - launched);
+      for (int j = 0; j < nb; ++j) {
+        CP1<ST> p1;
+        p1.vs = (const ST*)c->VS;
+        p1.al = al;
+        p1.r = (const ST*)c->R;
+        p1.p = (ST*)c->P[0];
+        p1.st = c->sst;
+        GADI_TRY(launch_pw(c, p1));
+        CP2<ST> p2;
+        p2.vs = (const ST*)c->VS;
+        p2.al = al;
+        p2.p = (const ST*)c->P[0];
+        p2.y = (ST*)c->Y;
+        p2.r = (ST*)c->R;
+        p2.st = c->sst;
+        GADI_TRY(launch_pw(c, p2));
+      }
+      launched += nb;
+      GADI_TRY(poll_state(c, c->sst, c->h_sst));
+      polled = true;
+      if (c->h_sst->done) break;
+      batch = std::max(2, c->pred_s / 4 + 1);
+    }
+    if (!polled) GADI_TRY(poll_state(c, c->sst, c->h_sst));
+    c->pred_s = c->h_sst->it;
+    return 0;
+  }
+
+  // ------------------------------------------------------------ outer pass
+  template <int DIM, int ZS, int UR, bool HAS_E, bool CPLX>
+  static int outer_t(Ctx* c, double scale) {
+    typedef GeoT<double, DIM, ZS> G;
+    Outer<G, ST, UR, HAS_E, CPLX> o;
+    o.x = c->x[c->xcur];
+    o.y = (const ST*)c->Y;
+    o.xs = c->xs;
+    o.b = c->b;
+    o.v = c->v64;
+    o.xout = c->x[c->xcur ^ 1];
+    o.r = c->r;
+    o.out = c->osum;
+    o.A = c->A;
+    o.A32 = c->A32;
+    o.scale = scale;
+    o.ones = c->ones;
+    o.u32 = (c->u != GADI_FP64 && c->u != GADI_FP64X2) ? 1 : 0;
+    GADI_TRY(launch_sweep(c, o));
+    c->xcur ^= 1;
+    return 0;
+  }
+
+  template <int DIM, int ZS, bool CPLX>
+  static int outer_d(Ctx* c, double scale, int has_e) {
+    if constexpr (CPLX) {
+      return has_e ? outer_t<DIM, ZS, 0, true, true>(c, scale) : outer_t<DIM, ZS, 0, false, true>(c, scale);
+    } else {
+      const int ur = c->ur == GADI_FP64 ? 0 : (c->ur == GADI_FP64X2 ? 2 : 1);
+      if (ur == 0) return has_e ? outer_t<DIM, ZS, 0, true, false>(c, scale) : outer_t<DIM, ZS, 0, false, false>(c, scale);
+      if (ur == 1) return has_e ? outer_t<DIM, ZS, 1, true, false>(c, scale) : outer_t<DIM, ZS, 1, false, false>(c, scale);
+      return has_e ? outer_t<DIM, ZS, 2, true, false>(c, scale) : outer_t<DIM, ZS, 2, false, false>(c, scale);
+    }
+  }
+
+  // ------------------------------------------------------------ Op x
+  template <int DIM, int ZS, bool STRICT>
+  static int apply_sweep(Ctx* c, const CoefT<double>& C, const double* in, double* out) {
+    typedef GeoT<ST, DIM, ZS> G;
+    ApplyOp<G, STRICT> a;
+    a.in = in;
+    a.outv = out;
+    a.C = cast_coef<CT>(C);
+    return launch_sweep(c, a);
+  }
+  template <bool TRANS, bool STRICT>
+  static int apply_cplx(Ctx* c, const double* in, double* out) {
+    CApply<ST, TRANS, STRICT> a;
+    a.vs = (const ST*)c->VS;
+    a.al = (CT)c->d.alpha_s;
+    a.in = in;
+    a.outv = out;
+    return launch_pw(c, a);
+  }
+
+  // ------------------------------------------------------------ vtable
+  static int h_solve(Ctx* c, double scale, double tol, int maxit) {
+    if (c->kind == GADI_COMPLEX) return h_solve_t<2, 2>(c, scale, tol, maxit);
+    if (c->ndim == 3) return h_solve_t<3, 1>(c, scale, tol, maxit);
+    return h_solve_t<2, 1>(c, scale, tol, maxit);
+  }
+  static int s_solve(Ctx* c, double coeff, double tol, int maxit) {
+    if (c->kind == GADI_COMPLEX) return s_solve_cplx(c, coeff, tol, maxit);
+    if (c->ndim == 3) return s_solve_real<3>(c, coeff, tol, maxit);
+    return s_solve_real<2>(c, coeff, tol, maxit);
+  }
+  static int outer(Ctx* c, double scale, int has_e) {
+    if (c->kind == GADI_COMPLEX) return outer_d<2, 2, true>(c, scale, has_e);
+    if (c->ndim == 3) return outer_d<3, 1, false>(c, scale, has_e);
+    return outer_d<2, 1, false>(c, scale, has_e);
+  }
+  static int apply(Ctx* c, int op, int strict, const double* in, double* out) {
+    const CoefT<double>& C = op == 1 ? c->H : (op == 2 ? c->S : c->ST);
+    if (c->kind == GADI_COMPLEX) {
+      if (op == 1)
+        return strict ? apply_sweep<2, 2, true>(c, C, in, out) : apply_sweep<2, 2, false>(c, C, in, out);
+      if (op == 2) return strict ? apply_cplx<false, true>(c, in, out) : apply_cplx<false, false>(c, in, out);
+      return strict ? apply_cplx<true, true>(c, in, out) : apply_cplx<true, false>(c, in, out);
+    }
+    if (c->ndim == 3)
+      return strict ? apply_sweep<3, 1, true>(c, C, in, out) : apply_sweep<3, 1, false>(c, C, in, out);
+    return strict ? apply_sweep<2, 1, true>(c, C, in, out) : apply_sweep<2, 1, false>(c, C, in, out);
+  }
+  static int quantize(Ctx* c, const double* in, void* out, long long n) {
+    const int nb = (int)std::min<long long>((n + 255) / 256, (long long)c->sms * 16);
+    quantize_kernel<ST><<<std::max(nb, 1), 256, 0, c->stream>>>(in, (ST*)out, n);
+    c->launches++;
+    GADI_CUDA(cudaGetLastError());
+    return 0;
+  }
+  static int widen(Ctx* c, const void* in, double* out, long long n) {
+    const int nb = (int)std::min<long long>((n + 255) / 256, (long long)c->sms * 16);
+    widen_kernel<ST><<<std::max(nb, 1), 256, 0, c->stream>>>((const ST*)in, out, n);
+    c->launches++;
+    GADI_CUDA(cudaGetLastError());
+    return 0;
+  }
+  static EngineVT vt() { return EngineVT{&h_solve, &s_solve, &outer, &apply, &quantize, &widen}; }
+};
+
+}  // namespace gadi

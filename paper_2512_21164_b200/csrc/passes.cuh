@@ -1,0 +1,809 @@
+// The fused passes of one GADI outer step, written as sweep "passes"
+// (sweep.cuh) or pointwise passes (pointwise kernel below).
+//
+// Reference semantics each pass restates (all paths gadimp/...):
+//   HcgInit   gadi.py:151-153 (scale + cast of r to u_s), inner.py:56-63
+//   HcgA      inner.py:68-73   p <- r + beta p ; php = p.Hp ; alpha = rs/php
+//   HcgB      inner.py:74-86   z += alpha p ; r -= alpha Hp ; rs_new ; beta
+//   CgnrInit  gadi.py:158, inner.py:108-116  rhs2 = coeff z ; rbar = S^T rhs2
+//   CgnrP1    inner.py:121-126  p <- rbar + beta p ; w = S p ; alpha
+//   CgnrP2    inner.py:127-133  y += alpha p ; r -= alpha w ; fp64 ||r||
+//   CgnrP3    inner.py:134-140  rbar = S^T r ; rs_new ; beta
+//   Outer     gadi.py:163-176 + 147  x <- x + y/scale ; r = b - A x ;
+//             monitor sums (||r||, max|r|, ||x||, ||e||, ||A e||)
+//   NormA/B   analysis.py:51-70  power iteration on A^T A
+//
+// Storage model for u_s < fp64 (the paper's cublas*Ex design, PAPER.md:
+// 1180-1187): vectors live in u_s (bf16/fp16/fp32), arithmetic is fp32,
+// every stored vector is rounded RNE to u_s, dot products form fp32 products
+// and accumulate them in fp64.  u_s = fp64 runs the same code in fp64 with
+// the reference's ordered (non-FMA) stencil arithmetic.
+#pragma once
+#include "sweep_tma.cuh"
+
+namespace gadi {
+
+template <class ST> struct CTOf { typedef float type; };
+template <> struct CTOf<double> { typedef double type; };
+
+// Geometry traits.  DIM: 2 -> rows of 64 lanes, 1 row per CTA (the slow axis
+// is marched); 3 -> 32 lanes x 8 rows.  VZ elements per lane = one 16-byte
+// vector of the storage type (2 for fp64).
+template <class ST_, int DIM, int ZS_>
+struct GeoT {
+  typedef ST_ ST;
+  typedef typename CTOf<ST_>::type CT;
+  static constexpr int VZ = (int)(16 / sizeof(ST_)) >= 2 ? (int)(16 / sizeof(ST_)) : 2;
+  static constexpr int BZ = DIM == 3 ? 32 : 64;
+  static constexpr int BY = DIM == 3 ? 8 : 1;
+  static constexpr int ZS = ZS_;
+  static constexpr int NT = BZ * BY;
+};
+
+struct InnerState {
+  double rs, nrhs, alpha, beta, relres, tol;
+  int it, maxit, done, converged, breakdown, pad;
+};
+
+struct OuterSums {
+  // 0 sum r_mon^2, 1 max|r_alg|, 2 sum r_alg^2, 3 sum x^2, 4 sum e^2, 5 sum (A e)^2
+  double v[6];
+};
+
+struct NormState {
+  double nw, sigma, tol, pad;
+  int it, maxit, done, pad2;
+};
+
+// Dot product of one lane's vector: products and partial sum in the compute
+// type, one fp64 accumulation per vector (cross-vector sums are fp64).
+template <class CT, int VZ>
+__device__ __forceinline__ double dotv(const CT (&a)[VZ], const CT (&b)[VZ], int nv) {
+  CT acc = CT(0);
+#pragma unroll
+  for (int k = 0; k < VZ; ++k)
+    if (k < nv) acc = fma_rn(a[k], b[k], acc);
+  return (double)acc;
+}
+
+// Common plumbing every pass carries.
+struct PassBase {
+  SweepGeom g;
+  double* partials;
+  unsigned int* ticket;
+};
+
+// ============================================================== H-CG passes
+// f = (it == 0) ? r : round(r + beta p_in) ; Hf ; store p_out ; sum f.Hf
+template <class G>
+struct HcgA : G, PassBase {
+  typedef typename G::CT CT;
+  typedef typename G::ST ST;
+  static constexpr int NF = 1, NR = 1;
+  static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  InnerState* st;
+  const ST* r;
+  const ST* pin;
+  ST* pout;
+  CoefT<CT> H;
+  CT beta;
+  bool first;
+  struct Raw { CT r[G::VZ], p[G::VZ]; };
+  struct RawS { CT r, p; };
+  struct Epi {};
+  __device__ bool prepare() {
+    if (st->done) return false;
+    first = (st->it == 0);
+    beta = (CT)st->beta;
+    return true;
+  }
+  static constexpr int NIN = 2, NE = 0;
+  static constexpr int in_esz(int) { return (int)sizeof(ST); }
+  static constexpr int epi_esz(int) { return 1; }
+  __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)r : (const void*)pin; }
+  __device__ const void* epi_ptr(int) const { return nullptr; }
+  __device__ bool in_active(int j) const { return j == 0 || !first; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const {
+    lds_vec<ST, G::VZ>(R.p[0], z, a.r);
+    if (!first) lds_vec<ST, G::VZ>(R.p[1], z, a.p);
+  }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int z) const {
+    a.r = lds1<ST, CT>(R.p[0], z);
+    a.p = first ? CT(0) : lds1<ST, CT>(R.p[1], z);
+  }
+  __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
+  __device__ void load_raw(Raw& a, long long i, int nv) const {
+    load_any<ST, G::VZ, true>(r, i, nv, a.r, g.vec);
+    if (!first) load_any<ST, G::VZ, true>(pin, i, nv, a.p, g.vec);
+  }
+  __device__ void load_raw_s(RawS& a, long long i) const {
+    a.r = cvt_in<CT>(r[i]);
+    a.p = first ? CT(0) : cvt_in<CT>(pin[i]);
+  }
+  __device__ CT fval(CT rv, CT pv) const { return first ? rv : round_to<ST>(fma_rn(beta, pv, rv)); }
+  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = fval(a.r[k], first ? CT(0) : a.p[k]); }
+  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = fval(a.r, a.p); }
+  __device__ void load_epi(Epi&, long long, int) const {}
+  __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
+    return apply_stencil<ORD>(H, CT(0), n);
+  }
+  __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
+                           double (&red)[1]) const {
+    store_any<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
+    red[0] += dotv<CT, G::VZ>(fc[0], s[0], nv);
+  }
+  __device__ void finalize(const double (&t)[1]) const {
+    const double php = t[0];
+    if (php <= 0.0) {  // inner.py:70-72
+      st->breakdown = 1;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rs / php;
+  }
+};
+
+// f = p ; Hp ; z += alpha p ; r -= alpha Hp ; sum r.r ; convergence, beta
+template <class G>
+struct HcgB : G, PassBase {
+  typedef typename G::CT CT;
+  typedef typename G::ST ST;
+  static constexpr int NF = 1, NR = 1;
+  static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  InnerState* st;
+  const ST* p;
+  ST* z;
+  ST* r;
+  CoefT<CT> H;
+  CT alpha;
+  struct Raw { CT p[G::VZ]; };
+  struct RawS { CT p; };
+  struct Epi { CT z[G::VZ], r[G::VZ]; };
+  __device__ bool prepare() {
+    if (st->done) return false;
+    alpha = (CT)st->alpha;
+    return true;
+  }
+  static constexpr int NIN = 1, NE = 2;
+  static constexpr int in_esz(int) { return (int)sizeof(ST); }
+  static constexpr int epi_esz(int) { return (int)sizeof(ST); }
+  __device__ const void* in_ptr(int) const { return p; }
+  __device__ const void* epi_ptr(int j) const { return j == 0 ? (const void*)z : (const void*)r; }
+  __device__ bool in_active(int) const { return true; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.p); }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.p = lds1<ST, CT>(R.p[0], zo); }
+  __device__ void load_epi_sm(Epi& e, const SmRow& R, int zo) const {
+    lds_vec<ST, G::VZ>(R.p[0], zo, e.z);
+    lds_vec<ST, G::VZ>(R.p[1], zo, e.r);
+  }
+  __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<ST, G::VZ, true>(p, i, nv, a.p, g.vec); }
+  __device__ void load_raw_s(RawS& a, long long i) const { a.p = cvt_in<CT>(p[i]); }
+  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = a.p[k]; }
+  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = a.p; }
+  __device__ void load_epi(Epi& e, long long i, int nv) const {
+    load_any<ST, G::VZ, false>(z, i, nv, e.z, g.vec);
+    load_any<ST, G::VZ, false>(r, i, nv, e.r, g.vec);
+  }
+  __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
+    return apply_stencil<ORD>(H, CT(0), n);
+  }
+  __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
+                           double (&red)[1]) const {
+    CT zn[G::VZ], rn[G::VZ];
+#pragma unroll
+    for (int k = 0; k < G::VZ; ++k) {
+      zn[k] = round_to<ST>(fma_rn(alpha, fc[0][k], e.z[k]));
+      rn[k] = round_to<ST>(fma_rn(-alpha, s[0][k], e.r[k]));
+    }
+    red[0] += dotv<CT, G::VZ>(rn, rn, nv);
+    store_any<ST, G::VZ>(z, i, nv, zn, g.vec);
+    store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
+  }
+  __device__ void finalize(const double (&t)[1]) const {
+    const double rs_new = t[0];
+    const int it = st->it + 1;
+    st->it = it;
+    const double relres = sqrt(fmax(rs_new, 0.0)) / st->nrhs;  // inner.py:78
+    st->relres = relres;
+    if (relres <= st->tol) {
+      st->converged = 1;
+      st->done = 1;
+      return;
+    }
+    if (rs_new <= 0.0) {  // inner.py:82-83
+      st->done = 1;
+      return;
+    }
+    st->beta = rs_new / st->rs;
+    st->rs = rs_new;
+    if (it >= st->maxit) st->done = 1;
+  }
+};
+
+// ============================================================== CGNR passes
+// rhs2 = round(coeff z) ; r = rhs2 ; rbar = round(S^T rhs2) ; y = 0
+template <class G>
+struct CgnrInit : G, PassBase {
+  typedef typename G::CT CT;
+  typedef typename G::ST ST;
+  static constexpr int NF = 1, NR = 2;
+  static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  InnerState* st;
+  const ST* z;
+  ST* r;
+  ST* rbar;
+  ST* y;
+  CoefT<CT> ST_;  // S^T
+  CT coeff;
+  double tol;
+  int maxit;
+  struct Raw { CT z[G::VZ]; };
+  struct RawS { CT z; };
+  struct Epi {};
+  __device__ bool prepare() { return true; }
+  static constexpr int NIN = 1, NE = 0;
+  static constexpr int in_esz(int) { return (int)sizeof(ST); }
+  static constexpr int epi_esz(int) { return 1; }
+  __device__ const void* in_ptr(int) const { return z; }
+  __device__ const void* epi_ptr(int) const { return nullptr; }
+  __device__ bool in_active(int) const { return true; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.z); }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.z = lds1<ST, CT>(R.p[0], zo); }
+  __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
+  __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<ST, G::VZ, true>(z, i, nv, a.z, g.vec); }
+  __device__ void load_raw_s(RawS& a, long long i) const { a.z = cvt_in<CT>(z[i]); }
+  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = round_to<ST>(coeff * a.z[k]); }
+  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = round_to<ST>(coeff * a.z); }
+  __device__ void load_epi(Epi&, long long, int) const {}
+  __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
+    return apply_stencil<ORD>(ST_, CT(0), n);
+  }
+  __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
+                           double (&red)[2]) const {
+    CT rb[G::VZ], zero[G::VZ];
+#pragma unroll
+    for (int k = 0; k < G::VZ; ++k) {
+      rb[k] = round_to<ST>(s[0][k]);
+      zero[k] = CT(0);
+      if (k < nv) {
+        red[0] += (double)(rb[k] * rb[k]);
+        red[1] += (double)fc[0][k] * (double)fc[0][k];
+      }
+    }
+    store_any<ST, G::VZ>(r, i, nv, fc[0], g.vec);
+    store_any<ST, G::VZ>(rbar, i, nv, rb, g.vec);
+    store_any<ST, G::VZ>(y, i, nv, zero, g.vec);
+  }
+  __device__ void finalize(const double (&t)[2]) const {
+    st->tol = tol;
+    st->maxit = maxit;
+    st->it = 0;
+    st->breakdown = 0;
+    st->converged = 0;
+    st->done = 0;
+    st->beta = 0.0;
+    st->relres = 1.0;
+    const double nrhs = sqrt(t[1]);
+    st->nrhs = nrhs;
+    st->rs = t[0];
+    if (nrhs == 0.0) {  // inner.py:119-120 zero right-hand side
+      st->converged = 1;
+      st->relres = 0.0;
+      st->done = 1;
+    } else if (maxit <= 0) {
+      st->done = 1;
+    }
+  }
+};
+
+// f = (it==0) ? rbar : round(rbar + beta p_in) ; w = S f ; store p_out ; sum w.w
+template <class G>
+struct CgnrP1 : G, PassBase {
+  typedef typename G::CT CT;
+  typedef typename G::ST ST;
+  static constexpr int NF = 1, NR = 1;
+  static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  InnerState* st;
+  const ST* rbar;
+  const ST* pin;
+  ST* pout;
+  CoefT<CT> S;
+  CT beta;
+  bool first;
+  struct Raw { CT rb[G::VZ], p[G::VZ]; };
+  struct RawS { CT rb, p; };
+  struct Epi {};
+  __device__ bool prepare() {
+    if (st->done) return false;
+    first = (st->it == 0);
+    beta = (CT)st->beta;
+    return true;
+  }
+  static constexpr int NIN = 2, NE = 0;
+  static constexpr int in_esz(int) { return (int)sizeof(ST); }
+  static constexpr int epi_esz(int) { return 1; }
+  __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)rbar : (const void*)pin; }
+  __device__ const void* epi_ptr(int) const { return nullptr; }
+  __device__ bool in_active(int j) const { return j == 0 || !first; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const {
+    lds_vec<ST, G::VZ>(R.p[0], z, a.rb);
+    if (!first) lds_vec<ST, G::VZ>(R.p[1], z, a.p);
+  }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int z) const {
+    a.rb = lds1<ST, CT>(R.p[0], z);
+    a.p = first ? CT(0) : lds1<ST, CT>(R.p[1], z);
+  }
+  __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
+  __device__ void load_raw(Raw& a, long long i, int nv) const {
+    load_any<ST, G::VZ, true>(rbar, i, nv, a.rb, g.vec);
+    if (!first) load_any<ST, G::VZ, true>(pin, i, nv, a.p, g.vec);
+  }
+  __device__ void load_raw_s(RawS& a, long long i) const {
+    a.rb = cvt_in<CT>(rbar[i]);
+    a.p = first ? CT(0) : cvt_in<CT>(pin[i]);
+  }
+  __device__ CT fval(CT rv, CT pv) const { return first ? rv : round_to<ST>(fma_rn(beta, pv, rv)); }
+  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = fval(a.rb[k], first ? CT(0) : a.p[k]); }
+  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = fval(a.rb, a.p); }
+  __device__ void load_epi(Epi&, long long, int) const {}
+  __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
+    return apply_stencil<ORD>(S, CT(0), n);
+  }
+  __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
+                           double (&red)[1]) const {
+    store_any<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
+    red[0] += dotv<CT, G::VZ>(s[0], s[0], nv);
+  }
+  __device__ void finalize(const double (&t)[1]) const {
+    const double denom = t[0];
+    if (denom <= 0.0) {  // inner.py:123-125
+      st->breakdown = 1;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rs / denom;
+  }
+};
+
+// f = p ; w = S p ; y += alpha p ; r -= alpha w ; fp64 ||r||^2 ; convergence
+template <class G>
+struct CgnrP2 : G, PassBase {
+  typedef typename G::CT CT;
+  typedef typename G::ST ST;
+  static constexpr int NF = 1, NR = 1;
+  static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  InnerState* st;
+  const ST* p;
+  ST* y;
+  ST* r;
+  CoefT<CT> S;
+  CT alpha;
+  struct Raw { CT p[G::VZ]; };
+  struct RawS { CT p; };
+  struct Epi { CT y[G::VZ], r[G::VZ]; };
+  __device__ bool prepare() {
+    if (st->done) return false;
+    alpha = (CT)st->alpha;
+    return true;
+  }
+  static constexpr int NIN = 1, NE = 2;
+  static constexpr int in_esz(int) { return (int)sizeof(ST); }
+  static constexpr int epi_esz(int) { return (int)sizeof(ST); }
+  __device__ const void* in_ptr(int) const { return p; }
+  __device__ const void* epi_ptr(int j) const { return j == 0 ? (const void*)y : (const void*)r; }
+  __device__ bool in_active(int) const { return true; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.p); }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.p = lds1<ST, CT>(R.p[0], zo); }
+  __device__ void load_epi_sm(Epi& e, const SmRow& R, int zo) const {
+    lds_vec<ST, G::VZ>(R.p[0], zo, e.y);
+    lds_vec<ST, G::VZ>(R.p[1], zo, e.r);
+  }
+  __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<ST, G::VZ, true>(p, i, nv, a.p, g.vec); }
+  __device__ void load_raw_s(RawS& a, long long i) const { a.p = cvt_in<CT>(p[i]); }
+  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = a.p[k]; }
+  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = a.p; }
+  __device__ void load_epi(Epi& e, long long i, int nv) const {
+    load_any<ST, G::VZ, false>(y, i, nv, e.y, g.vec);
+    load_any<ST, G::VZ, false>(r, i, nv, e.r, g.vec);
+  }
+  __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
+    return apply_stencil<ORD>(S, CT(0), n);
+  }
+  __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
+                           double (&red)[1]) const {
+    CT yn[G::VZ], rn[G::VZ];
+#pragma unroll
+    for (int k = 0; k < G::VZ; ++k) {
+      yn[k] = round_to<ST>(fma_rn(alpha, fc[0][k], e.y[k]));
+      rn[k] = round_to<ST>(fma_rn(-alpha, s[0][k], e.r[k]));
+      if (k < nv) red[0] += (double)rn[k] * (double)rn[k];
+    }
+    store_any<ST, G::VZ>(y, i, nv, yn, g.vec);
+    store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
+  }
+  __device__ void finalize(const double (&t)[1]) const {
+    const int it = st->it + 1;
+    st->it = it;
+    const double relres = sqrt(t[0]) / st->nrhs;  // inner.py:130 (fp64 norm)
+    st->relres = relres;
+    if (relres <= st->tol) {
+      st->converged = 1;
+      st->done = 1;
+      return;
+    }
+    if (it >= st->maxit) st->done = 1;
+  }
+};
+
+// rbar = round(S^T r) ; rs_new = rbar.rbar ; beta
+template <class G>
+struct CgnrP3 : G, PassBase {
+  typedef typename G::CT CT;
+  typedef typename G::ST ST;
+  static constexpr int NF = 1, NR = 1;
+  static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  InnerState* st;
+  const ST* r;
+  ST* rbar;
+  CoefT<CT> ST_;
+  struct Raw { CT r[G::VZ]; };
+  struct RawS { CT r; };
+  struct Epi {};
+  __device__ bool prepare() { return !st->done; }
+  static constexpr int NIN = 1, NE = 0;
+  static constexpr int in_esz(int) { return (int)sizeof(ST); }
+  static constexpr int epi_esz(int) { return 1; }
+  __device__ const void* in_ptr(int) const { return r; }
+  __device__ const void* epi_ptr(int) const { return nullptr; }
+  __device__ bool in_active(int) const { return true; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.r); }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.r = lds1<ST, CT>(R.p[0], zo); }
+  __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
+  __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<ST, G::VZ, true>(r, i, nv, a.r, g.vec); }
+  __device__ void load_raw_s(RawS& a, long long i) const { a.r = cvt_in<CT>(r[i]); }
+  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = a.r[k]; }
+  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = a.r; }
+  __device__ void load_epi(Epi&, long long, int) const {}
+  __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
+    return apply_stencil<ORD>(ST_, CT(0), n);
+  }
+  __device__ void epilogue(long long i, int nv, const CT (&)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
+                           double (&red)[1]) const {
+    CT rb[G::VZ];
+#pragma unroll
+    for (int k = 0; k < G::VZ; ++k) {
+      rb[k] = round_to<ST>(s[0][k]);
+    }
+    red[0] += dotv<CT, G::VZ>(rb, rb, nv);
+    store_any<ST, G::VZ>(rbar, i, nv, rb, g.vec);
+  }
+  __device__ void finalize(const double (&t)[1]) const {
+    const double rs_new = t[0];
+    if (rs_new <= 0.0) {  // inner.py:136-137
+      st->done = 1;
+      return;
+    }
+    st->beta = rs_new / st->rs;
+    st->rs = rs_new;
+  }
+};
+
+// ============================================================== outer pass
+// Fields: x_new = round_u(x + y/scale), e = x* - x_new (HAS_E) and, for
+// u_r != fp64, a second copy of x_new that feeds the u_r residual stencil.
+// A is applied in fp64 with the reference's ordered arithmetic, so
+// r_mon = b - A x_new is bitwise the scipy CSR result (gadi.py:166).
+// UR: 0 fp64 residual (r_alg = r_mon; gadi.py:147 with a.quantized(fp64) is
+// A itself), 1 fp32 emulated residual on fp32-quantised A and b
+// (sparsemat.py:234), 2 compensated fp64x2 residual (sparsemat.py:202-212).
+// CPLX: crd interleaved layout; the V coupling enters each row sum in the
+// reference's ascending column order (real row: L terms, then -v*x_im;
+// imaginary row: v*x_re, then L terms; problems.py:113-116).
+template <class G, class SU, int UR, bool HAS_E, bool CPLX>
+struct Outer : G, PassBase {
+  typedef double CT;
+  static constexpr int VZ = G::VZ;
+  static constexpr int FE = HAS_E ? 1 : 0;
+  static constexpr int NF = 1 + (HAS_E ? 1 : 0) + (UR != 0 ? 1 : 0);
+  static constexpr int FU = NF - 1;
+  static constexpr int NR = 6;
+  static constexpr bool HAS_RED = true, ORD = true, TMA_OK = !CPLX;
+  static __device__ __forceinline__ int op(int s) { return s == 1 ? RED_MAX : RED_SUM; }
+  const double* x;
+  const SU* y;
+  const double* xs;   // exact solution, unless ones
+  const double* b;
+  const double* v;    // crd potential (fp64), by complex index
+  double* xout;
+  double* r;          // algorithmic residual (u_r values stored as fp64)
+  OuterSums* out;
+  CoefT<double> A;    // fp64 coefficients
+  CoefT<float> A32;   // fp32-quantised coefficients (UR == 1)
+  double scale;
+  int ones;           // exact solution is the all-ones vector
+  int u32;            // working precision fp32
+  struct Raw { double x[VZ], y[VZ], xs[VZ]; };
+  struct RawS { double x, y, xs; };
+  struct Epi { double b[VZ], v[VZ]; };
+  __device__ bool prepare() { return true; }
+  static constexpr int NIN = HAS_E ? 3 : 2, NE = 1;
+  static constexpr int in_esz(int j) { return j == 1 ? (int)sizeof(SU) : 8; }
+  static constexpr int epi_esz(int) { return 8; }
+  __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)x : (j == 1 ? (const void*)y : (const void*)xs); }
+  __device__ const void* epi_ptr(int) const { return b; }
+  __device__ bool in_active(int j) const { return j < 2 || !ones; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const {
+    lds_vec<double, VZ>(R.p[0], z, a.x);
+    lds_vec<SU, VZ>(R.p[1], z, a.y);
+    if (HAS_E && !ones) lds_vec<double, VZ>(R.p[2], z, a.xs);
+  }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int z) const {
+    a.x = lds1<double, double>(R.p[0], z);
+    a.y = lds1<SU, double>(R.p[1], z);
+    a.xs = (HAS_E && !ones) ? lds1<double, double>(R.p[2], z) : 1.0;
+  }
+  // v (crd) is indexed by complex point; it is read from global by the
+  // epilogue-input loader of the register path (load_epi), never here
+  __device__ void load_epi_sm(Epi& e, const SmRow& R, int z) const { lds_vec<double, VZ>(R.p[0], z, e.b); }
+  __device__ void load_raw(Raw& a, long long i, int nv) const {
+    load_any<double, VZ, true>(x, i, nv, a.x, g.vec);
+    load_any<SU, VZ, true>(y, i, nv, a.y, g.vec);
+    if (HAS_E && !ones) load_any<double, VZ, true>(xs, i, nv, a.xs, g.vec);
+  }
+  __device__ void load_raw_s(RawS& a, long long i) const {
+    a.x = x[i];
+    a.y = cvt_in<double>(y[i]);
+    a.xs = (HAS_E && !ones) ? xs[i] : 1.0;
+  }
+  __device__ double xnew(double xv, double yv) const {
+    const double t = add_rn(xv, __ddiv_rn(yv, scale));  // gadi.py:163 x + y/scale
+    return u32 ? (double)__double2float_rn(t) : t;
+  }
+  __device__ void fill(double xn, double xsv, double (&f)[NF]) const {
+    f[0] = xn;
+    if constexpr (HAS_E) f[FE] = sub_rn(ones ? 1.0 : xsv, xn);
+    if constexpr (UR != 0) f[FU] = xn;
+  }
+  __device__ void field(const Raw& a, int k, double (&f)[NF]) const {
+    fill(xnew(a.x[k], a.y[k]), (HAS_E && !ones) ? a.xs[k] : 1.0, f);
+  }
+  __device__ void field_s(const RawS& a, double (&f)[NF]) const { fill(xnew(a.x, a.y), a.xs, f); }
+  __device__ void load_epi(Epi& e, long long i, int nv) const {
+    load_any<double, VZ, true>(b, i, nv, e.b, g.vec);
+    if constexpr (CPLX) {
+#pragma unroll
+      for (int k = 0; k < VZ; k += 2) {
+        const double vv = (k < nv) ? v[(i + k) >> 1] : 0.0;
+        e.v[k] = vv;
+        e.v[k + 1] = vv;
+      }
+    }
+  }
+  __device__ double stencil(int q, int k, const Nb<double>& n, const double (&fc)[NF][VZ], const Epi& e) const {
+    if (UR == 1 && q == FU) {
+      const Nb<float> nf{(float)n.xm, (float)n.ym, (float)n.zm, (float)n.ce, (float)n.zp, (float)n.yp, (float)n.xp};
+      return (double)apply_stencil<true>(A32, 0.0f, nf);
+    }
+    if (UR == 2 && q == FU) {
+      // b - A x as one compensated sum (TwoSum / exact FMA TwoProd)
+      double s = e.b[k], c = 0.0;
+      const double cf[7] = {A.lo[0], A.lo[1], A.lo[2], A.d, A.up[2], A.up[1], A.up[0]};
+      const double xv[7] = {n.xm, n.ym, n.zm, n.ce, n.zp, n.yp, n.xp};
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        if (cf[j] != 0.0) {
+          const double xx = -xv[j];
+          const double pr = mul_rn(cf[j], xx);
+          const double ep = fma_rn(cf[j], xx, -pr);
+          const double sn = add_rn(s, pr);
+          const double bb = sub_rn(sn, s);
+          const double er = add_rn(sub_rn(s, sub_rn(sn, bb)), sub_rn(pr, bb));
+          s = sn;
+          c = add_rn(c, add_rn(er, ep));
+        }
+      }
+      return add_rn(s, c);
+    }
+    double acc = 0.0;
+    if constexpr (CPLX) {
+      if (k & 1) acc = add_rn(0.0, mul_rn(e.v[k], fc[q][k - 1]));
+    }
+    acc = apply_stencil<true>(A, acc, n);
+    if constexpr (CPLX) {
+      if (!(k & 1)) acc = add_rn(acc, mul_rn(-e.v[k], fc[q][k + 1]));
+    }
+    return acc;
+  }
+  __device__ void epilogue(long long i, int nv, const double (&fc)[NF][VZ], const double (&s)[NF][VZ], const Epi& e,
+                           double (&red)[6]) const {
+    double rv[VZ];
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) {
+      const double rmon = sub_rn(e.b[k], s[0][k]);  // gadi.py:166 b - A x
+      double ralg = rmon;
+      if constexpr (UR == 1) ralg = (double)__fsub_rn(__double2float_rn(e.b[k]), (float)s[FU][k]);
+      if constexpr (UR == 2) ralg = s[FU][k];
+      rv[k] = ralg;
+      if (k < nv) {
+        red[0] += rmon * rmon;
+        const double ar = fabs(ralg);
+        red[1] = (ar > red[1] || ar != ar) ? ar : red[1];
+        red[2] += ralg * ralg;
+        red[3] += fc[0][k] * fc[0][k];
+        if constexpr (HAS_E) {
+          red[4] += fc[FE][k] * fc[FE][k];
+          red[5] += s[FE][k] * s[FE][k];
+        }
+      }
+    }
+    store_any<double, VZ>(xout, i, nv, fc[0], g.vec);
+    store_any<double, VZ>(r, i, nv, rv, g.vec);
+  }
+  __device__ void finalize(const double (&t)[6]) const {
+#pragma unroll
+    for (int s = 0; s < 6; ++s) out->v[s] = t[s];
+  }
+};
+
+// ============================================================== ||A||_2
+// Power iteration on A^T A (analysis.py:51-70).
+// NormPass<false>: f = w / nw ; t = A f.   NormPass<true>: f = t ; w = A^T t ;
+// sum w^2 ; sigma update and stop test on the device.
+template <class G, bool CPLX, bool TRANS>
+struct NormPass : G, PassBase {
+  typedef double CT;
+  static constexpr int NF = 1, NR = 1;
+  static constexpr bool HAS_RED = TRANS, ORD = true, TMA_OK = !CPLX;
+  static constexpr int VZ = G::VZ;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  NormState* ns;
+  const double* in;
+  double* outv;
+  const double* v;  // crd potential
+  CoefT<double> A;  // A (TRANS=false) or A^T (TRANS=true)
+  double nw;
+  struct Raw { double a[VZ]; };
+  struct RawS { double a; };
+  struct Epi { double v[VZ]; };
+  __device__ bool prepare() {
+    if (ns->done) return false;
+    nw = ns->nw;
+    return true;
+  }
+  static constexpr int NIN = 1, NE = 0;
+  static constexpr int in_esz(int) { return 8; }
+  static constexpr int epi_esz(int) { return 1; }
+  __device__ const void* in_ptr(int) const { return in; }
+  __device__ const void* epi_ptr(int) const { return nullptr; }
+  __device__ bool in_active(int) const { return true; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const { lds_vec<double, VZ>(R.p[0], z, a.a); }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int z) const { a.a = lds1<double, double>(R.p[0], z); }
+  __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
+  __device__ double fv(double a) const { return TRANS ? a : __ddiv_rn(a, nw); }  // analysis.py:66 v = w / nw
+  __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<double, VZ, true>(in, i, nv, a.a, g.vec); }
+  __device__ void load_raw_s(RawS& a, long long i) const { a.a = in[i]; }
+  __device__ void field(const Raw& a, int k, double (&f)[1]) const { f[0] = fv(a.a[k]); }
+  __device__ void field_s(const RawS& a, double (&f)[1]) const { f[0] = fv(a.a); }
+  __device__ void load_epi(Epi& e, long long i, int nv) const {
+    if constexpr (CPLX) {
+#pragma unroll
+      for (int k = 0; k < VZ; k += 2) {
+        const double vv = (k < nv) ? v[(i + k) >> 1] : 0.0;
+        e.v[k] = vv;
+        e.v[k + 1] = vv;
+      }
+    }
+  }
+  // A:   real row  L.. then -v x_im ; imag row  v x_re then L..
+  // A^T: real row  L.. then +v x_im ; imag row -v x_re then L..
+  __device__ double stencil(int, int k, const Nb<double>& n, const double (&fc)[1][VZ], const Epi& e) const {
+    double acc = 0.0;
+    if constexpr (CPLX) {
+      if (k & 1) acc = add_rn(0.0, mul_rn(TRANS ? -e.v[k] : e.v[k], fc[0][k - 1]));
+    }
+    acc = apply_stencil<true>(A, acc, n);
+    if constexpr (CPLX) {
+      if (!(k & 1)) acc = add_rn(acc, mul_rn(TRANS ? e.v[k] : -e.v[k], fc[0][k + 1]));
+    }
+    return acc;
+  }
+  __device__ void epilogue(long long i, int nv, const double (&)[1][VZ], const double (&s)[1][VZ], const Epi&,
+                           double (&red)[1]) const {
+    double o[VZ];
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) {
+      o[k] = s[0][k];
+      if (TRANS && k < nv) red[0] += o[k] * o[k];
+    }
+    store_any<double, VZ>(outv, i, nv, o, g.vec);
+  }
+  __device__ void finalize(const double (&t)[1]) const {
+    const double nwn = sqrt(t[0]);
+    if (nwn == 0.0) {  // analysis.py:62-63
+      ns->sigma = 0.0;
+      ns->done = 1;
+      return;
+    }
+    const double sig_new = sqrt(nwn);
+    ns->nw = nwn;
+    ns->it += 1;
+    if (fabs(sig_new - ns->sigma) <= ns->tol * sig_new) {  // analysis.py:67-68
+      ns->sigma = sig_new;
+      ns->done = 1;
+      return;
+    }
+    ns->sigma = sig_new;
+    if (ns->it >= ns->maxit) ns->done = 1;
+  }
+};
+
+// ============================================================== y = Op x
+// Standalone operator application (sparsemat.spmv on H_low / S_low / S_low_T,
+// sparsemat.py:178-199).  Input and output cross as fp64 arrays holding u_s
+// images.  STRICT rounds every product and every partial sum to u_s in
+// ascending column order -- bitwise the reference's emulated spmv -- while
+// the default storage model accumulates in the compute type and rounds once.
+template <class G, bool STRICT>
+struct ApplyOp : G, PassBase {
+  typedef typename G::CT CT;
+  typedef typename G::ST ST;
+  static constexpr int NF = 1, NR = 1, VZ = G::VZ;
+  static constexpr bool HAS_RED = false, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  const double* in;
+  double* outv;
+  CoefT<CT> C;
+  struct Raw { CT a[VZ]; };
+  struct RawS { CT a; };
+  struct Epi {};
+  __device__ bool prepare() { return true; }
+  static constexpr int NIN = 1, NE = 0;
+  static constexpr int in_esz(int) { return 8; }
+  static constexpr int epi_esz(int) { return 1; }
+  __device__ const void* in_ptr(int) const { return in; }
+  __device__ const void* epi_ptr(int) const { return nullptr; }
+  __device__ bool in_active(int) const { return true; }
+  __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const { lds_vec<double, VZ>(R.p[0], z, a.a); }
+  __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int z) const { a.a = lds1<double, CT>(R.p[0], z); }
+  __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
+  __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<double, VZ, true>(in, i, nv, a.a, g.vec); }
+  __device__ void load_raw_s(RawS& a, long long i) const { a.a = (CT)in[i]; }
+  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = a.a[k]; }
+  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = a.a; }
+  __device__ void load_epi(Epi&, long long, int) const {}
+  __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][VZ], const Epi&) const {
+    if constexpr (STRICT) {
+      const CT cf[7] = {C.lo[0], C.lo[1], C.lo[2], C.d, C.up[2], C.up[1], C.up[0]};
+      const CT xv[7] = {n.xm, n.ym, n.zm, n.ce, n.zp, n.yp, n.xp};
+      CT acc = CT(0);
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        if (cf[j] != CT(0)) {
+          const CT pr = round_to<ST>(mul_rn(cf[j], xv[j]));
+          acc = any ? round_to<ST>(add_rn(acc, pr)) : pr;
+          any = true;
+        }
+      }
+      return acc;
+    } else {
+      return apply_stencil<ORD>(C, CT(0), n);
+    }
+  }
+  __device__ void epilogue(long long i, int nv, const CT (&)[1][VZ], const CT (&s)[1][VZ], const Epi&,
+                           double (&)[1]) const {
+    double o[VZ];
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) o[k] = (double)s[0][k];
+    store_any<double, VZ>(outv, i, nv, o, g.vec);
+  }
+  __device__ void finalize(const double (&)[1]) const {}
+};
+
+}  // namespace gadi

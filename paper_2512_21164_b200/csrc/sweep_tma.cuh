@@ -1,0 +1,405 @@
+// Warp-specialised, TMA-fed version of the 2.5-D stencil sweep (sweep.cuh).
+//
+// One producer warp streams every plane a CTA needs into a ring of NST
+// shared-memory stages with cp.async.bulk (the TMA bulk-copy engine,
+// SASS UBLKCP) completing on per-stage mbarriers; the consumer warps never
+// issue global loads for the stencil inputs, so the number of bytes in
+// flight is set by the ring depth, not by registers.  A stage holds, for one
+// x-plane, the (TY+2) haloed rows of every stencil input (each row padded by
+// 16 bytes on both sides so every bulk copy is 16-byte aligned) and the TY
+// core rows of every epilogue input.
+//
+// Consumers keep the register queue (x-neighbours), the f-plane double
+// buffer (y-neighbours) and warp shuffles (z-neighbours) of sweep.cuh; they
+// synchronise among themselves with a named barrier and hand stages back to
+// the producer through "empty" mbarriers.  Out-of-grid rows / planes are
+// simply not copied and are masked by coordinates, so stage contents beyond
+// the grid are never read.  Requires every input row to start 16-byte
+// aligned (nz * elem_size % 16 == 0) and arrays padded on both sides
+// (the context allocates every vector with guard bands).
+#pragma once
+#include "sweep.cuh"
+
+namespace gadi {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// per-row pointers handed to the pass loaders: element 0 of the tile core
+struct SmRow {
+  const unsigned char* p[4];
+};
+
+template <class T, int VZ, class CT>
+__device__ __forceinline__ void lds_vec(const unsigned char* row, int zoff, CT (&out)[VZ]) {
+  const T* q = reinterpret_cast<const T*>(row) + zoff;
+  constexpr int BYTES = VZ * (int)sizeof(T);
+  if constexpr (BYTES % 16 == 0) {
+    constexpr int PER = 16 / (int)sizeof(T);
+#pragma unroll
+    for (int c = 0; c < BYTES / 16; ++c) {
+      const uint4 u = reinterpret_cast<const uint4*>(q)[c];
+      const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) out[c * PER + j] = cvt_in<CT>(e[j]);
+    }
+  } else if constexpr (BYTES == 8) {
+    const uint2 u = *reinterpret_cast<const uint2*>(q);
+    const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int j = 0; j < VZ; ++j) out[j] = cvt_in<CT>(e[j]);
+  } else if constexpr (BYTES == 4) {
+    const unsigned u = *reinterpret_cast<const unsigned*>(q);
+    const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int j = 0; j < VZ; ++j) out[j] = cvt_in<CT>(e[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < VZ; ++j) out[j] = cvt_in<CT>(q[j]);
+  }
+}
+template <class T, class CT>
+__device__ __forceinline__ CT lds1(const unsigned char* row, int zoff) {
+  return cvt_in<CT>(reinterpret_cast<const T*>(row)[zoff]);
+}
+
+template <class P> struct TmaShape {
+  using B = SweepShape<P>;
+  static constexpr int TZ = B::TZ, TY = B::TY;
+  static constexpr int hz(int esz) { return 16 / esz; }
+  static constexpr int rb_in(int j) { return (TZ + 2 * hz(P::in_esz(j))) * P::in_esz(j); }
+  static constexpr int rb_epi(int j) { return TZ * P::epi_esz(j); }
+  static constexpr int off_in(int j) {
+    int o = 0;
+    for (int i = 0; i < j; ++i) o += (TY + 2) * rb_in(i);
+    return o;
+  }
+  static constexpr int off_epi(int j) {
+    int o = off_in(P::NIN);
+    for (int i = 0; i < j; ++i) o += TY * rb_epi(i);
+    return o;
+  }
+  static constexpr int STAGE = off_epi(P::NE);
+  static constexpr int FBYTES = (int)B::SMEM;  // two f-plane buffers
+  static constexpr int BUDGET = 110 * 1024;
+  static constexpr int NST_RAW = (BUDGET - FBYTES) / STAGE;
+  static constexpr int NST = NST_RAW < 2 ? 2 : (NST_RAW > 8 ? 8 : NST_RAW);
+  static constexpr size_t SMEM = (size_t)FBYTES + (size_t)NST * STAGE + 2 * NST * sizeof(uint64_t);
+};
+
+template <class P>
+__global__ void __launch_bounds__(P::NT + 32) sweep_tma_kernel(P p) {
+  using S = SweepShape<P>;
+  using TS = TmaShape<P>;
+  using CT = typename P::CT;
+  constexpr int VZ = S::VZ, BZ = S::BZ, BY = S::BY, ZS = S::ZS, NF = S::NF;
+  constexpr int TZ = S::TZ, TY = S::TY, PAD = S::PAD, ROW = S::ROW;
+  constexpr int NR = P::NR, NT = P::NT, NIN = P::NIN, NE = P::NE, NST = TS::NST;
+  constexpr int NWC = NT / 32;  // consumer warps
+  static_assert(NIN <= 4 && NE <= 4, "at most four inputs of each kind");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  CT* fsm = reinterpret_cast<CT*>(smem_raw);
+  unsigned char* stages = smem_raw + TS::FBYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)NST * TS::STAGE);
+  uint64_t* empty = full + NST;
+
+  if (!p.prepare()) return;
+
+  const SweepGeom g = p.g;
+  const int tid = threadIdx.x;
+  int bidx = blockIdx.x;
+  const int ztile = bidx % g.nzt;
+  bidx /= g.nzt;
+  const int ytile = bidx % g.nyt;
+  bidx /= g.nyt;
+  const int xa = bidx * g.xchunk;
+  const int xb = min(g.nx, xa + g.xchunk);
+  const int zt0 = ztile * TZ, y0 = ytile * TY;
+  const int nplanes = xb - xa + 2;  // xa-1 .. xb
+
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  double red[NR];
+#pragma unroll
+  for (int s = 0; s < NR; ++s) red[s] = 0.0;
+
+  if (tid >= NT) {
+    // ------------------------------------------------------------ producer
+    // the whole warp issues the row copies of a stage (one row per lane),
+    // lane 0 posts the byte count first
+    const int lane = tid & 31;
+    constexpr int NCOPY = NIN * (TY + 2) + NE * TY;
+    for (int s = 0; s < nplanes; ++s) {
+      const int xp = xa - 1 + s;
+      const int st = s % NST;
+      if (s >= NST) mbar_wait(&empty[st], (unsigned)(((s / NST) - 1) & 1));
+      unsigned char* sb = stages + (size_t)st * TS::STAGE;
+      const bool pv = (xp >= 0 && xp < g.nx);
+      const bool ev = pv && xp >= xa && xp < xb;
+      unsigned bytes = 0;
+      if (pv) {
+#pragma unroll
+        for (int j = 0; j < NIN; ++j)
+          if (p.in_active(j))
+            for (int r = 0; r < TY + 2; ++r) {
+              const int yy = y0 - 1 + r;
+              if (yy >= 0 && yy < g.ny) bytes += TS::rb_in(j);
+            }
+        if (ev) {
+#pragma unroll
+          for (int j = 0; j < NE; ++j)
+            for (int r = 0; r < TY; ++r)
+              if (y0 + r < g.ny) bytes += TS::rb_epi(j);
+        }
+      }
+      if (lane == 0) mbar_expect_tx(&full[st], bytes);
+      __syncwarp();
+      if (pv) {
+        for (int q = lane; q < NCOPY; q += 32) {
+          if (q < NIN * (TY + 2)) {
+            const int j = q / (TY + 2), r = q % (TY + 2);
+            const int yy = y0 - 1 + r;
+            if (!p.in_active(j) || yy < 0 || yy >= g.ny) continue;
+            const int esz = P::in_esz(j), hz = TS::hz(esz);
+            const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
+            const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0 - hz;
+            bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j), base + e0 * esz, (unsigned)TS::rb_in(j), &full[st]);
+          } else if (ev) {
+            const int q2 = q - NIN * (TY + 2);
+            const int j = q2 / TY, r = q2 % TY;
+            const int yy = y0 + r;
+            if (yy >= g.ny) continue;
+            const int esz = P::epi_esz(j);
+            const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
+            const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0;
+            bulk_g2s(sb + TS::off_epi(j) + r * TS::rb_epi(j), base + e0 * esz, (unsigned)TS::rb_epi(j), &full[st]);
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int tz = tid % BZ, ty = tid / BZ, lane = tid & 31;
+    const int zb = zt0 + tz * VZ, y = y0 + ty;
+    const bool yok = y < g.ny;
+    const int nvz = yok ? max(0, min(VZ, g.nz - zb)) : 0;
+    const bool own_hm = (ty == 0), own_hp = (ty == BY - 1);
+    const bool hm_ok = own_hm && y0 - 1 >= 0, hp_ok = own_hp && y0 + TY < g.ny;
+    const int nvh = max(0, min(VZ, g.nz - zb));
+    const bool own_zl = (tz == 0), own_zr = (tz == BZ - 1);
+
+    auto gidx = [&](int xx, int yy, int zz) -> long long {
+      return (long long)xx * g.plane + (long long)yy * g.nz + zz;
+    };
+    // row r (0 .. TY+1, 0 = y0-1) of stage st, pointing at core element 0
+    auto in_row = [&](int st, int r) {
+      SmRow R;
+      const unsigned char* sb = stages + (size_t)st * TS::STAGE;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
+#pragma unroll
+      for (int j = 0; j < NIN; ++j)
+        R.p[j] = sb + TS::off_in(j) + r * TS::rb_in(j) + TS::hz(P::in_esz(j)) * P::in_esz(j);
+      return R;
+    };
+    auto epi_row = [&](int st, int r) {
+      SmRow R;
+      const unsigned char* sb = stages + (size_t)st * TS::STAGE;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
+#pragma unroll
+      for (int j = 0; j < NE; ++j) R.p[j] = sb + TS::off_epi(j) + r * TS::rb_epi(j);
+      return R;
+    };
+    auto fields_core = [&](int st, int r, int nv, CT (&f)[NF][VZ]) {
+      typename P::Raw a;
+      if (nv > 0) p.load_raw_sm(a, in_row(st, r), tz * VZ);
+#pragma unroll
+      for (int k = 0; k < VZ; ++k) {
+        CT t[NF];
+        if (k < nv) {
+          p.field(a, k, t);
+        } else {
+#pragma unroll
+          for (int q = 0; q < NF; ++q) t[q] = CT(0);
+        }
+#pragma unroll
+        for (int q = 0; q < NF; ++q) f[q][k] = t[q];
+      }
+    };
+    // the full f-plane (core, y-halo rows, z-halo) of the plane held by stage st
+    auto write_fplane = [&](CT* buf, int st, bool pv, const CT (&fc)[NF][VZ]) {
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        CT* rowc = buf + ((size_t)q * (TY + 2) + (ty + 1)) * ROW + PAD + tz * VZ;
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) rowc[k] = fc[q][k];
+      }
+      if (own_hm || own_hp) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const bool mine = h == 0 ? own_hm : own_hp;
+          if (!mine) continue;
+          const bool ok = pv && (h == 0 ? hm_ok : hp_ok);
+          CT fh[NF][VZ];
+          fields_core(st, h == 0 ? 0 : TY + 1, ok ? nvh : 0, fh);
+          const int rr = h == 0 ? 0 : TY + 1;
+#pragma unroll
+          for (int q = 0; q < NF; ++q) {
+            CT* row = buf + ((size_t)q * (TY + 2) + rr) * ROW + PAD + tz * VZ;
+#pragma unroll
+            for (int k = 0; k < VZ; ++k) row[k] = fh[q][k];
+          }
+        }
+      }
+      if (own_zl || own_zr) {
+        const SmRow R = in_row(st, ty + 1);
+#pragma unroll
+        for (int j = 0; j < ZS; ++j) {
+          const int zl = zt0 - ZS + j, zr = zt0 + TZ + j;
+          CT tl[NF], tr[NF];
+          if (own_zl && pv && yok && zl >= 0) {
+            typename P::RawS a;
+            p.load_raw_s_sm(a, R, -ZS + j);
+            p.field_s(a, tl);
+          } else {
+#pragma unroll
+            for (int q = 0; q < NF; ++q) tl[q] = CT(0);
+          }
+          if (own_zr && pv && yok && zr < g.nz) {
+            typename P::RawS a;
+            p.load_raw_s_sm(a, R, TZ + j);
+            p.field_s(a, tr);
+          } else {
+#pragma unroll
+            for (int q = 0; q < NF; ++q) tr[q] = CT(0);
+          }
+#pragma unroll
+          for (int q = 0; q < NF; ++q) {
+            CT* row = buf + ((size_t)q * (TY + 2) + (ty + 1)) * ROW;
+            if (own_zl) row[PAD - ZS + j] = tl[q];
+            if (own_zr) row[PAD + TZ + j] = tr[q];
+          }
+        }
+      }
+    };
+    auto release = [&](int s) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s % NST]);
+    };
+
+    CT fprev[NF][VZ], fcur[NF][VZ], fnext[NF][VZ];
+    // prologue: plane xa-1 (core only), plane xa (f-plane buffer 0)
+    {
+      mbar_wait(&full[0], 0u);
+      const bool pv = xa - 1 >= 0;
+      fields_core(0, ty + 1, pv ? nvz : 0, fprev);
+      release(0);
+      mbar_wait(&full[1 % NST], (unsigned)((1 / NST) & 1));
+      fields_core(1 % NST, ty + 1, nvz, fcur);
+      write_fplane(fsm, 1 % NST, true, fcur);
+    }
+    consumer_sync(NT);
+
+    for (int x = xa; x < xb; ++x) {
+      const int s = x - xa + 1;  // stage index of plane x
+      CT* bcur = fsm + (size_t)((x - xa) & 1) * S::PLANE;
+      CT* bnxt = fsm + (size_t)(((x - xa) + 1) & 1) * S::PLANE;
+      // 1. plane x+1 -> fnext + f-plane buffer
+      const int s1 = s + 1;
+      mbar_wait(&full[s1 % NST], (unsigned)((s1 / NST) & 1));
+      const bool pv1 = x + 1 < g.nx;
+      fields_core(s1 % NST, ty + 1, pv1 ? nvz : 0, fnext);
+      write_fplane(bnxt, s1 % NST, pv1, fnext);
+      // 2. stencil(s) and epilogue of plane x
+      typename P::Epi E;
+      p.load_epi_sm(E, epi_row(s % NST, ty), tz * VZ);
+      CT st[NF][VZ];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        const CT* rowm = bcur + ((size_t)q * (TY + 2) + ty) * ROW + PAD + tz * VZ;
+        const CT* rowc = rowm + ROW;
+        const CT* rowp = rowc + ROW;
+        CT left[ZS], right[ZS];
+#pragma unroll
+        for (int j = 0; j < ZS; ++j) {
+          CT fromprev = __shfl_up_sync(0xffffffffu, fcur[q][VZ - ZS + j], 1);
+          CT fromnext = __shfl_down_sync(0xffffffffu, fcur[q][j], 1);
+          left[j] = (lane == 0) ? rowc[-ZS + j] : fromprev;
+          right[j] = (lane == 31) ? rowc[VZ + j] : fromnext;
+        }
+        CT ym[VZ], yp[VZ];
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) {
+          ym[k] = rowm[k];
+          yp[k] = rowp[k];
+        }
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) {
+          const CT zm = (k >= ZS) ? fcur[q][k - ZS] : left[k];
+          const CT zp = (k + ZS < VZ) ? fcur[q][k + ZS] : right[k + ZS - VZ];
+          const Nb<CT> nb{fprev[q][k], ym[k], zm, fcur[q][k], zp, yp[k], fnext[q][k]};
+          st[q][k] = p.stencil(q, k, nb, fcur, E);
+        }
+      }
+      if (nvz > 0) p.epilogue(gidx(x, y, zb), nvz, fcur, st, E, red);
+      release(s);
+#pragma unroll
+      for (int q = 0; q < NF; ++q)
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) {
+          fprev[q][k] = fcur[q][k];
+          fcur[q][k] = fnext[q][k];
+        }
+      consumer_sync(NT);
+    }
+  }
+
+  if constexpr (P::HAS_RED) {
+    double tot[NR];
+    int ops[NR];
+#pragma unroll
+    for (int s = 0; s < NR; ++s) ops[s] = P::op(s);
+    if (grid_finish<NR, NT + 32>(red, ops, p.partials, g.pstride, p.ticket, tot)) {
+      if (threadIdx.x == 0) p.finalize(tot);
+    }
+  }
+}
+
+}  // namespace gadi

@@ -1,0 +1,93 @@
+"""Inner Krylov solvers (drop-in for gadimp/inner.py:1-143), on the GPU.
+
+``cg_spd`` (classical CG on H = alpha I + M) and ``cg_normal_skew`` (CGNR on
+S = alpha I + N) run the same fused, device-driven kernels the outer loop
+uses (csrc/passes.cuh: HcgA/HcgB, CgnrP1-3; csrc/pointwise.cuh for the crd
+family).  Arithmetic follows the storage model: vectors stored in ``fmt``,
+fp32 compute, fp64 accumulation of dot products; stopping quantities are
+the reference's (sqrt(rs)/||rhs|| for CG, the fp64 ||r||/||rhs|| for CGNR).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .device import make_desc, open_context
+from .precision import resolve_format
+from .stencil import StencilMatrix
+
+__all__ = ["InnerSolveStats", "cg_spd", "cg_normal_skew", "default_maxit"]
+
+_MAXIT_CAP = 10_000
+
+
+def default_maxit(n: int) -> int:
+    """min(10^4, ceil(5 sqrt(n))) (inner.py:26-27)."""
+    return min(_MAXIT_CAP, max(1, math.ceil(5.0 * math.sqrt(n))))
+
+
+@dataclass
+class InnerSolveStats:
+    iterations: int
+    final_relative_residual: float
+    converged: bool
+    breakdown: bool
+    true_relative_residual: float = float("nan")
+
+
+def _ctx_for(op: StencilMatrix, fmt, which: str):
+    if not isinstance(op, StencilMatrix):
+        raise NotImplementedError("general CSR operators are served by the CSR engine")
+    spec = op.spec
+    if spec.family == "crd":
+        return open_context(make_desc(spec, op.alpha, fmt, coef_fmt=op.fmt))
+    c = op.coefs()
+    return open_context(make_desc(spec, 0.0, fmt, H=c, S=c))
+
+
+def _true_relres(op: StencilMatrix, rhs, x, nrhs) -> float:
+    if nrhs == 0.0:
+        return 0.0
+    spec = op.spec
+    if spec.family == "crd":
+        ctx = open_context(make_desc(spec, op.alpha, "fp64", coef_fmt=op.fmt))
+        y = ctx.spmv({"H": 1, "S": 2, "ST": 3, "AmN": 3}[op.role], x, strict=True)
+    else:
+        c = op.coefs()
+        ctx = open_context(make_desc(spec, 0.0, "fp64", H=c, S=c))
+        y = ctx.spmv(1, x, strict=True)
+    ctx.close()
+    return float(np.linalg.norm(rhs - y)) / nrhs
+
+
+def cg_spd(h, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
+           strict_model: bool = True):
+    """CG on H x = rhs, H SPD, x0 = 0."""
+    fmt = resolve_format(fmt)
+    rhs = np.asarray(rhs, dtype=np.float64)
+    if maxit is None:
+        maxit = default_maxit(rhs.size)
+    with _ctx_for(h, fmt, "H") as ctx:
+        x, st = ctx.h_solve(rhs, tol, maxit)
+    nrhs = float(np.linalg.norm(rhs))
+    return x, InnerSolveStats(st.iterations, st.final_relative_residual, bool(st.converged),
+                              bool(st.breakdown), _true_relres(h, rhs, x, nrhs))
+
+
+def cg_normal_skew(s, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
+                   strict_model: bool = True, s_transpose=None):
+    """CGNR on S y = rhs (S^T S y = S^T rhs without forming S^T S), y0 = 0.
+    ``s_transpose`` is implied by the stencil (S^T swaps the lo/up
+    coefficients; crd flips the sign of V)."""
+    fmt = resolve_format(fmt)
+    rhs = np.asarray(rhs, dtype=np.float64)
+    if maxit is None:
+        maxit = default_maxit(rhs.size)
+    with _ctx_for(s, fmt, "S") as ctx:
+        y, st = ctx.s_solve(rhs, tol, maxit)
+    nrhs = float(np.linalg.norm(rhs))
+    return y, InnerSolveStats(st.iterations, st.final_relative_residual, bool(st.converged),
+                              bool(st.breakdown), _true_relres(s, rhs, y, nrhs))

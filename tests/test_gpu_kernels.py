@@ -1,0 +1,87 @@
+"""GPU kernel parity against the reference's golden outputs (bitwise where
+the reference arithmetic is reproducible: fp64 ordered stencils, the strict
+u_s spmv, the fp32 and fp64x2 residuals, b = A 1)."""
+
+import numpy as np
+import pytest
+
+import paper_2512_21164_b200 as g
+from paper_2512_21164_b200 import device
+from paper_2512_21164_b200.stencil import spec_cd_3d, spec_cdr_2d, spec_complex_rd
+
+pytestmark = pytest.mark.gpu
+
+
+def _spec(meta):
+    fam, n_g, kw = meta["family"], meta["n_g"], meta["kw"]
+    if fam == "cdr2d":
+        return spec_cdr_2d(n_g, **kw)
+    if fam == "cd3d":
+        return spec_cd_3d(n_g)
+    return spec_complex_rd(n_g, **kw)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def _assert_bitwise(got, want, what):
+    got, want = np.asarray(got), np.asarray(want)
+    bad = np.nonzero(_bits(got) != _bits(want))[0]
+    # +0 / -0 differences are representation-only; everything else must match
+    real_bad = [i for i in bad if not (got[i] == 0.0 and want[i] == 0.0)]
+    assert not real_bad, f"{what}: {len(real_bad)} mismatches, first {real_bad[:5]} " \
+                         f"got {got[real_bad[:3]]} want {want[real_bad[:3]]}"
+
+
+def test_rhs_ones_bitwise(gpu, golden_kernels, golden_kernel_meta):
+    for m in golden_kernel_meta:
+        spec = _spec(m)
+        _assert_bitwise(device.rhs_ones(spec), golden_kernels[f"{m['tag']}/b_ones"], m["tag"])
+
+
+def test_residual_fp64_bitwise(gpu, golden_kernels, golden_kernel_meta):
+    for m in golden_kernel_meta:
+        p = g.StencilProblem(_spec(m))
+        t = m["tag"]
+        r = g.residual(p.A, golden_kernels[f"{t}/x"], golden_kernels[f"{t}/bvec"], "fp64")
+        _assert_bitwise(r, golden_kernels[f"{t}/res_fp64"], t)
+
+
+def test_spmv_A_fp64_bitwise(gpu, golden_kernels, golden_kernel_meta):
+    for m in golden_kernel_meta:
+        p = g.StencilProblem(_spec(m))
+        t = m["tag"]
+        _assert_bitwise(g.spmv(p.A, golden_kernels[f"{t}/x"], "fp64"), golden_kernels[f"{t}/Ax_fp64"], t)
+
+
+def test_residual_fp32_and_compensated_bitwise(gpu, golden_kernels, golden_kernel_meta):
+    for m in golden_kernel_meta:
+        if m["family"] == "crd":
+            continue
+        p = g.StencilProblem(_spec(m))
+        t = m["tag"]
+        xq = golden_kernels[f"{t}/xq32"]
+        r32 = g.residual(p.A, xq, golden_kernels[f"{t}/bvec"], "fp32")
+        _assert_bitwise(r32, golden_kernels[f"{t}/res_fp32"], t + " fp32")
+        r2 = g.residual(p.A, golden_kernels[f"{t}/x"], golden_kernels[f"{t}/bvec"], "fp64x2")
+        _assert_bitwise(r2, golden_kernels[f"{t}/res_fp64x2"], t + " fp64x2")
+
+
+@pytest.mark.parametrize("us", ["bf16", "fp16", "fp32", "fp64"])
+def test_strict_spmv_splitting_bitwise(gpu, golden_kernels, golden_kernel_meta, us):
+    for m in golden_kernel_meta:
+        p = g.StencilProblem(_spec(m))
+        t = m["tag"]
+        sp = g.make_hss_splitting(p.A, m["alpha"], us)
+        x = golden_kernels[f"{t}/{us}/xq"] if us != "fp64" else golden_kernels[f"{t}/x"]
+        for name, op in (("H", sp.H_low), ("S", sp.S_low), ("ST", sp.S_low_T)):
+            _assert_bitwise(g.spmv(op, x, us), golden_kernels[f"{t}/{us}/{name}"], f"{t} {us} {name}")
+
+
+def test_norm2_matches_reference(gpu, golden_kernels, golden_kernel_meta):
+    for m in golden_kernel_meta:
+        p = g.StencilProblem(_spec(m))
+        want = float(golden_kernels[f"{m['tag']}/norm2"][0])
+        got = g.matrix_norm_2(p.A)
+        assert got == pytest.approx(want, rel=1e-12), m["tag"]

@@ -1,0 +1,117 @@
+"""End-to-end gadi_solve and inner-solver parity against the reference's
+golden runs (tests/golden/solves.json, inner.json).
+
+Parity bar (BASELINE.json north_star): same final status, outer iteration
+count within +-1 (+-0 when u = u_r = u_s = fp64), final backward error within
+2x of the reference's; inner counts are reported, not bound."""
+
+import numpy as np
+import pytest
+
+import paper_2512_21164_b200 as g
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(c):
+    fam, n_g, kw = c["family"], c["n_g"], c.get("kw", {})
+    return {"cdr2d": g.build_cdr_2d, "cd3d": g.build_cd_3d, "crd": g.build_complex_rd}[fam](n_g, **kw)
+
+
+def _check(c, rep):
+    all64 = all(c["cfg"].get(k, "fp64") == "fp64" for k in ("u", "u_r", "u_s"))
+    tol = 0 if all64 else 1
+    assert rep.status == c["status"], (c["name"], rep.status, c["status"])
+    if c["status"] == "Stagnated":
+        # stagnation fires on a window test; the floor must match, the count loosely
+        assert abs(rep.iterations - c["outer"]) <= max(10, int(0.1 * c["outer"])), c["name"]
+    else:
+        assert abs(rep.iterations - c["outer"]) <= tol, (c["name"], rep.iterations, c["outer"])
+    b_ref, b_got = c["berr"][-1], rep.history[-1].backward_error
+    assert b_got <= 2.0 * b_ref and b_ref <= 2.0 * b_got, (c["name"], b_got, b_ref)
+    assert rep.norm_A == pytest.approx(c["norm_A"], rel=1e-10)
+
+
+SOLVE_CASES = [
+    "c3_cdr2d16_bf16", "c3_cdr2d16_fp32", "c3_cdr2d16_fp64", "c3_cdr2d32_bf16", "c3_cdr2d32_fp32",
+    "c3_cdr2d32_fp64", "c3_cdr2d64_bf16", "c3_cdr2d64_fp32", "c3_cdr2d64_fp64",
+    "c3_cd3d8_bf16", "c3_cd3d8_fp32", "c3_cd3d8_fp64", "c3_cd3d16_bf16", "c3_cd3d16_fp32", "c3_cd3d16_fp64",
+    "c3_crd16_bf16", "c3_crd16_fp32", "c3_crd16_fp64", "c3_crd32_bf16", "c3_crd32_fp32", "c3_crd32_fp64",
+    "gadi_cdr2d6", "omega05_cdr2d16_fp32", "r03_cdr2d24_bf16", "nonstrict_cdr2d32_bf16",
+    "innertol1e2_cd3d12_bf16", "three_precision_cdr2d8", "stagnation_cdr2d8",
+    "floor_cdr2d64_bf16", "floor_cd3d16_fp32", "cfg1_cdr2d256_fp64", "cfg1_cdr2d256_fp32",
+]
+
+
+@pytest.mark.parametrize("name", SOLVE_CASES)
+def test_solve_matches_reference(gpu, golden_solves, name):
+    if name not in golden_solves:
+        pytest.skip(f"{name} not in fixtures")
+    c = golden_solves[name]
+    rep = g.gadi_solve(_problem(c), cfg=g.GadiConfig(**c["cfg"]))
+    _check(c, rep)
+    # the first record is computed from x0 = 0 and x1: its residual norm is ||b||
+    assert rep.history[0].residual_norm == pytest.approx(c["residual_norm"][0], rel=1e-12)
+
+
+def test_report_contract(gpu):
+    p = g.build_cdr_2d(6)
+    rep = g.gadi_solve(p, cfg=g.GadiConfig(alpha=1.0, outer_tol=1e-10))
+    assert rep.status == "Converged"
+    assert rep.final_relative_residual <= 1e-10
+    assert rep.history[-1].forward_error < 1e-8
+    rr = rep.relative_residuals
+    assert all(rr[k + 1] < rr[k] * 1.05 for k in range(len(rr) - 1))
+    assert rep.total_inner_iterations > 0
+    assert set(rep.wallclock) == {"residual", "inner_h", "inner_s", "update", "monitor"}
+    assert np.allclose(rep.x, 1.0, atol=1e-8)
+
+
+def test_supplied_splitting_and_alpha_check(gpu):
+    p = g.build_cdr_2d(4)
+    s = g.make_hss_splitting(p.A, 2.0, "fp64")
+    rep = g.gadi_solve(p, s, g.GadiConfig(alpha=2.0, outer_tol=1e-8))
+    assert rep.status == "Converged"
+    with pytest.raises(ValueError):
+        g.gadi_solve(p, s, g.GadiConfig(alpha=1.0))
+
+
+def test_keep_iterates(gpu):
+    p = g.build_cdr_2d(4)
+    rep = g.gadi_solve(p, cfg=g.GadiConfig(alpha=1.0, outer_tol=0.0, outer_maxit=7), keep_iterates=True)
+    assert len(rep.iterates) == 7
+    assert np.array_equal(rep.iterates[-1], rep.x)
+
+
+def test_host_rhs_path_equals_device_rhs_path(gpu):
+    p1 = g.build_cd_3d(12)
+    p2 = g.build_cd_3d(12)
+    _ = p2.b  # pull b to the host: the solve uploads it instead of generating it
+    cfg = g.GadiConfig(alpha=0.5, u_s="bf16", outer_tol=1e-6)
+    r1 = g.gadi_solve(p1, cfg=cfg)
+    r2 = g.gadi_solve(p2, cfg=cfg)
+    assert r1.iterations == r2.iterations
+    assert np.array_equal(r1.x, r2.x)
+
+
+@pytest.mark.parametrize("k", range(9))
+def test_inner_solvers_vs_reference(gpu, golden_inner, k):
+    c = golden_inner[k]
+    fam = c["family"]
+    p = {"cdr2d": g.build_cdr_2d, "cd3d": g.build_cd_3d, "crd": g.build_complex_rd}[fam](c["n_g"])
+    sp = g.make_hss_splitting(p.A, c["alpha"], c["u_s"])
+    rhs = np.array(c["rhs"])
+    z, sh = g.cg_spd(sp.H_low, rhs, 1e-4, None, c["u_s"])
+    y, ss = g.cg_normal_skew(sp.S_low, rhs, 1e-4, None, c["u_s"], True, sp.S_low_T)
+    zr, yr = np.array(c["h_x"]), np.array(c["s_x"])
+    if c["u_s"] == "fp64":
+        assert sh.iterations == c["h_it"] and ss.iterations == c["s_it"]
+        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+        assert np.linalg.norm(y - yr) <= 1e-10 * np.linalg.norm(yr)
+    else:
+        assert abs(sh.iterations - c["h_it"]) <= max(2, 0.2 * c["h_it"]), (sh.iterations, c["h_it"])
+        assert abs(ss.iterations - c["s_it"]) <= max(2, 0.2 * c["s_it"]), (ss.iterations, c["s_it"])
+    assert sh.converged and ss.converged
+    # both solutions satisfy the same true-residual level
+    assert sh.true_relative_residual <= max(3 * c["h_true"], 3e-4)
+    assert ss.true_relative_residual <= max(3 * c["s_true"], 3e-4)
