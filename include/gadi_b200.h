@@ -161,6 +161,16 @@ int gadi_spmv(gadi_ctx* ctx, int op, int strict, const double* x, double* y);
  * (sparsemat.py:219-234).  Clobbers the solver iterate. */
 int gadi_residual(gadi_ctx* ctx, const double* x, double* r);
 
+/* Live per-kernel device timers (CUDA events on the context stream around
+ * every launch while enabled).  kid: 0 H-CG init, 1 H-CG pass A, 2 H-CG
+ * pass B, 3 CGNR init, 4-6 CGNR passes 1-3, 7-9 crd CGNR init/P1/P2,
+ * 10 outer pass, 11-12 ||A||_2 passes, 13 operator apply.  Enabling resets. */
+int gadi_prof_enable(gadi_ctx* ctx, int on);
+int gadi_prof_read(gadi_ctx* ctx, int kid, double* total_ms, int64_t* launches);
+/* device time between two points on the context stream */
+int gadi_timer_start(gadi_ctx* ctx);
+int gadi_timer_stop(gadi_ctx* ctx, double* ms);
+
 /* elapsed device ms of the last gadi_norm2 call */
 double gadi_last_norm_ms(gadi_ctx* ctx);
 /* number of device kernels this context has launched */

@@ -98,6 +98,10 @@ SIGNATURES = {
     "gadi_s_solve": (C.c_int, [_VP, _DP, C.c_double, C.c_int, _DP, C.POINTER(InnerStats)]),
     "gadi_spmv": (C.c_int, [_VP, C.c_int, C.c_int, _DP, _DP]),
     "gadi_residual": (C.c_int, [_VP, _DP, _DP]),
+    "gadi_prof_enable": (C.c_int, [_VP, C.c_int]),
+    "gadi_prof_read": (C.c_int, [_VP, C.c_int, _DP, C.POINTER(C.c_int64)]),
+    "gadi_timer_start": (C.c_int, [_VP]),
+    "gadi_timer_stop": (C.c_int, [_VP, _DP]),
     "gadi_last_norm_ms": (C.c_double, [_VP]),
     "gadi_kernel_launches": (C.c_int64, [_VP]),
 }
@@ -262,6 +266,29 @@ class Context:
         r = np.empty(self.n)
         check(self._L.gadi_residual(self.h, dptr(x), dptr(r)))
         return r
+
+    KERNELS = ["hcg_init", "hcg_a", "hcg_b", "cgnr_init", "cgnr_p1", "cgnr_p2", "cgnr_p3",
+               "crd_init", "crd_p1", "crd_p2", "outer", "norm_a", "norm_b", "apply"]
+
+    def prof_enable(self, on=True):
+        check(self._L.gadi_prof_enable(self.h, 1 if on else 0))
+
+    def prof_read(self) -> dict:
+        out = {}
+        for k, name in enumerate(self.KERNELS):
+            ms, n = C.c_double(0.0), C.c_int64(0)
+            check(self._L.gadi_prof_read(self.h, k, C.byref(ms), C.byref(n)))
+            if n.value:
+                out[name] = (float(ms.value), int(n.value))
+        return out
+
+    def timer_start(self):
+        check(self._L.gadi_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_double(0.0)
+        check(self._L.gadi_timer_stop(self.h, C.byref(ms)))
+        return float(ms.value)
 
     def last_norm_ms(self) -> float:
         return float(self._L.gadi_last_norm_ms(self.h))

@@ -114,6 +114,7 @@ static void free_ctx(Ctx* c) {
     if (p) cudaFreeHost(p);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->evpool) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -363,7 +364,7 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
   GADI_CUDA(cudaSetDevice(c->device));
   double* w = c->x[0];
   double* t = c->x[1];
-  GADI_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  GADI_CUDA(cudaEventRecord(c->ev[6], c->stream));
   if (v0) {
     GADI_TRY(upload(c, v0, w));
   } else {
@@ -387,6 +388,7 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
     launched += nb;
     GADI_CUDA(cudaMemcpyAsync(c->h_nst, c->nst, sizeof(NormState), cudaMemcpyDeviceToHost, c->stream));
     GADI_CUDA(cudaStreamSynchronize(c->stream));
+    prof_collect(c);
     polled = true;
     if (c->h_nst->done) break;
     batch = 128;
@@ -395,10 +397,10 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
     GADI_CUDA(cudaMemcpyAsync(c->h_nst, c->nst, sizeof(NormState), cudaMemcpyDeviceToHost, c->stream));
     GADI_CUDA(cudaStreamSynchronize(c->stream));
   }
-  GADI_CUDA(cudaEventRecord(c->ev[5], c->stream));
-  GADI_CUDA(cudaEventSynchronize(c->ev[5]));
+  GADI_CUDA(cudaEventRecord(c->ev[7], c->stream));
+  GADI_CUDA(cudaEventSynchronize(c->ev[7]));
   float ms = 0.f;
-  GADI_CUDA(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]));
+  GADI_CUDA(cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]));
   c->last_norm_ms = ms;
   *sigma = c->h_nst->sigma;
   if (iterations) *iterations = c->h_nst->it;
@@ -453,6 +455,7 @@ int gadi_outer_step(gadi_ctx* h, const gadi_step_args* a, gadi_outer_scalars* ou
   GADI_CUDA(cudaEventRecord(c->ev[3], c->stream));
   GADI_CUDA(cudaMemcpyAsync(c->h_osum, c->osum, sizeof(OuterSums), cudaMemcpyDeviceToHost, c->stream));
   GADI_CUDA(cudaStreamSynchronize(c->stream));
+  prof_collect(c);
   if (out) fill_scalars(c->h_osum, out);
   if (hs) fill_stats(c->h_hst, hs);
   if (ss) fill_stats(c->h_sst, ss);
@@ -524,6 +527,45 @@ int gadi_residual(gadi_ctx* h, const double* x, double* r) {
   GADI_CUDA(cudaMemsetAsync(c->Y, 0, c->ssz * (size_t)c->n, c->stream));
   GADI_TRY(c->vt->outer(c, 1.0, 0));  // x_new = x + 0 ; r = b - A x
   return download(c, c->r, r);
+}
+
+int gadi_prof_enable(gadi_ctx* h, int on) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  prof_collect(c);
+  c->prof = on ? 1 : 0;
+  for (int k = 0; k < K_NKID; ++k) {
+    c->prof_ms[k] = 0.0;
+    c->prof_n[k] = 0;
+  }
+  return 0;
+}
+
+int gadi_prof_read(gadi_ctx* h, int kid, double* total_ms, int64_t* launches) {
+  Ctx* c = &h->c;
+  if (kid < 0 || kid >= K_NKID) return set_error("kernel id out of range", GADI_ERR_ARG);
+  GADI_CUDA(cudaStreamSynchronize(c->stream));
+  prof_collect(c);
+  *total_ms = c->prof_ms[kid];
+  *launches = c->prof_n[kid];
+  return 0;
+}
+
+int gadi_timer_start(gadi_ctx* h) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  return 0;
+}
+
+int gadi_timer_stop(gadi_ctx* h, double* ms) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaEventRecord(c->ev[5], c->stream));
+  GADI_CUDA(cudaEventSynchronize(c->ev[5]));
+  float m = 0.f;
+  GADI_CUDA(cudaEventElapsedTime(&m, c->ev[4], c->ev[5]));
+  *ms = m;
+  return 0;
 }
 
 double gadi_last_norm_ms(gadi_ctx* h) { return h->c.last_norm_ms; }

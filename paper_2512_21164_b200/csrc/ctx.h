@@ -63,7 +63,7 @@ struct Ctx {
   OuterSums* h_osum = nullptr;
   NormState* h_nst = nullptr;
 
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
   int has_exact = 0, ones = 0;
   int pred_h = 4, pred_s = 4;  // iteration-count predictions for launch batching
   long long launches = 0;
@@ -71,6 +71,15 @@ struct Ctx {
   int waves = 1;      // grid size in waves of resident CTAs (TMA sweep)
   int min_chunk = 8;  // lower bound on planes per CTA
   double last_norm_ms = 0.0;
+
+  // live per-kernel timers: event pairs around every launch while enabled,
+  // folded into per-kernel totals at each host synchronisation point
+  int prof = 0;
+  std::vector<cudaEvent_t> evpool;
+  std::vector<int> evkid;
+  int evused = 0;
+  double prof_ms[K_NKID] = {};
+  long long prof_n[K_NKID] = {};
 
   CoefT<double> A, AT, H, S, ST;
   CoefT<float> A32;
@@ -146,6 +155,36 @@ inline SweepGeom make_geom(const Ctx* c, int TZ, int TY, int VZ, long long slots
 }
 inline int geom_blocks(const SweepGeom& g) {
   return g.nzt * g.nyt * ((g.nx + g.xchunk - 1) / g.xchunk);
+}
+
+inline void prof_begin(Ctx* c, int kid) {
+  if (!c->prof) return;
+  if ((size_t)(2 * c->evused + 2) > c->evpool.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->evpool.push_back(e);
+    }
+    c->evkid.resize(c->evpool.size() / 2);
+  }
+  c->evkid[c->evused] = kid;
+  cudaEventRecord(c->evpool[2 * c->evused], c->stream);
+}
+inline void prof_end(Ctx* c) {
+  if (!c->prof) return;
+  cudaEventRecord(c->evpool[2 * c->evused + 1], c->stream);
+  c->evused++;
+}
+// call after the stream has been synchronised
+inline void prof_collect(Ctx* c) {
+  for (int i = 0; i < c->evused; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->evpool[2 * i], c->evpool[2 * i + 1]) == cudaSuccess) {
+      c->prof_ms[c->evkid[i]] += ms;
+      c->prof_n[c->evkid[i]] += 1;
+    }
+  }
+  c->evused = 0;
 }
 
 extern EngineVT engine_bf16, engine_fp16, engine_fp32, engine_fp64;

@@ -43,7 +43,9 @@ inline int launch_sweep(Ctx* c, P& p) {
     p.g = make_geom(c, S::TZ, S::TY, P::VZ, (long long)occ * c->sms);
     const int nb = geom_blocks(p.g);
     if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
+    prof_begin(c, P::KID);
     sweep_tma_kernel<P><<<nb, P::NT + 32, smem, c->stream>>>(p);
+    prof_end(c);
   } else {
     p.g = make_geom(c, S::TZ, S::TY, P::VZ);
     const int nb = geom_blocks(p.g);
@@ -56,7 +58,9 @@ inline int launch_sweep(Ctx* c, P& p) {
         attr = true;
       }
     }
+    prof_begin(c, P::KID);
     sweep_kernel<P><<<nb, P::NT, smem, c->stream>>>(p);
+    prof_end(c);
   }
   c->launches++;
   GADI_CUDA(cudaGetLastError());
@@ -72,7 +76,9 @@ inline int launch_pw(Ctx* c, P& p) {
   const long long chunks = (c->n + (long long)PW_NT * P::VZ - 1) / ((long long)PW_NT * P::VZ);
   int nb = (int)std::min<long long>(chunks, (long long)c->sms * 8);
   nb = std::max(nb, 1);
+  prof_begin(c, P::KID);
   pointwise_kernel<P><<<nb, PW_NT, 0, c->stream>>>(p);
+  prof_end(c);
   c->launches++;
   GADI_CUDA(cudaGetLastError());
   return 0;
@@ -88,6 +94,7 @@ inline int launch_pw(Ctx* c, P& p) {
 inline int poll_state(Ctx* c, InnerState* dev, InnerState* host) {
   GADI_CUDA(cudaMemcpyAsync(host, dev, sizeof(InnerState), cudaMemcpyDeviceToHost, c->stream));
   GADI_CUDA(cudaStreamSynchronize(c->stream));
+  prof_collect(c);
   return 0;
 }
 

@@ -40,6 +40,12 @@ struct GeoT {
   static constexpr int NT = BZ * BY;
 };
 
+// Kernel ids for the live per-kernel timers (gadi_prof_*).
+enum KernelId {
+  K_HCG_INIT = 0, K_HCG_A, K_HCG_B, K_CGNR_INIT, K_CGNR_P1, K_CGNR_P2, K_CGNR_P3,
+  K_C_INIT, K_C_P1, K_C_P2, K_OUTER, K_NORM_A, K_NORM_B, K_APPLY, K_NKID
+};
+
 struct InnerState {
   double rs, nrhs, alpha, beta, relres, tol;
   int it, maxit, done, converged, breakdown, pad;
@@ -81,6 +87,7 @@ struct HcgA : G, PassBase {
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int KID = K_HCG_A;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
   const ST* r;
@@ -151,6 +158,7 @@ struct HcgB : G, PassBase {
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int KID = K_HCG_B;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
   const ST* p;
@@ -230,6 +238,7 @@ struct CgnrInit : G, PassBase {
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 2;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int KID = K_CGNR_INIT;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
   const ST* z;
@@ -306,6 +315,7 @@ struct CgnrP1 : G, PassBase {
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int KID = K_CGNR_P1;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
   const ST* rbar;
@@ -376,6 +386,7 @@ struct CgnrP2 : G, PassBase {
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int KID = K_CGNR_P2;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
   const ST* p;
@@ -447,6 +458,7 @@ struct CgnrP3 : G, PassBase {
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int KID = K_CGNR_P3;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
   const ST* r;
@@ -514,6 +526,7 @@ struct Outer : G, PassBase {
   static constexpr int FU = NF - 1;
   static constexpr int NR = 6;
   static constexpr bool HAS_RED = true, ORD = true, TMA_OK = !CPLX;
+  static constexpr int KID = K_OUTER;
   static __device__ __forceinline__ int op(int s) { return s == 1 ? RED_MAX : RED_SUM; }
   const double* x;
   const SU* y;
@@ -661,6 +674,7 @@ struct NormPass : G, PassBase {
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = TRANS, ORD = true, TMA_OK = !CPLX;
   static constexpr int VZ = G::VZ;
+  static constexpr int KID = TRANS ? K_NORM_B : K_NORM_A;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   NormState* ns;
   const double* in;
@@ -755,6 +769,7 @@ struct ApplyOp : G, PassBase {
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1, VZ = G::VZ;
   static constexpr bool HAS_RED = false, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int KID = K_APPLY;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   const double* in;
   double* outv;

@@ -59,6 +59,7 @@ struct HcgInit : PwBase {
   static constexpr int VZ = (int)(16 / sizeof(ST)) >= 2 ? (int)(16 / sizeof(ST)) : 2;
   static constexpr int NR = 2;
   static constexpr bool HAS_RED = true;
+  static constexpr int KID = K_HCG_INIT;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   const double* r64;
   ST* rs;
@@ -152,6 +153,7 @@ struct CInit : CplxBase<ST> {
   typedef typename B::CT CT;
   static constexpr int VZ = B::VZ, NR = 2;
   static constexpr bool HAS_RED = true;
+  static constexpr int KID = K_C_INIT;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   const ST* z;
   ST* r;
@@ -202,6 +204,7 @@ struct CP1 : CplxBase<ST> {
   typedef typename B::CT CT;
   static constexpr int VZ = B::VZ, NR = 1;
   static constexpr bool HAS_RED = true;
+  static constexpr int KID = K_C_P1;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   const ST* r;
   ST* p;
@@ -250,6 +253,7 @@ struct CP2 : CplxBase<ST> {
   typedef typename B::CT CT;
   static constexpr int VZ = B::VZ, NR = 2;
   static constexpr bool HAS_RED = true;
+  static constexpr int KID = K_C_P2;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   const ST* p;
   ST* y;
@@ -314,6 +318,7 @@ struct CApply : CplxBase<ST> {
   typedef typename B::CT CT;
   static constexpr int VZ = B::VZ, NR = 1;
   static constexpr bool HAS_RED = false;
+  static constexpr int KID = K_APPLY;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   const double* in;
   double* outv;
