@@ -14,7 +14,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libgadi_b200.so"
+LIB_PATH = Path(os.environ.get("GADI_LIB", Path(__file__).resolve().parent / "libgadi_b200.so"))
 CSRC = Path(__file__).resolve().parent / "csrc"
 
 GADI_OK, GADI_ERR_CUDA, GADI_ERR_ARG, GADI_ERR_OOM, GADI_ERR_UNSUPPORTED = 0, 1, 2, 3, 4

@@ -185,6 +185,7 @@ int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out) {
   c->no_tma = getenv("GADI_NO_TMA") ? atoi(getenv("GADI_NO_TMA")) : 0;
   if (getenv("GADI_WAVES")) c->waves = std::max(1, atoi(getenv("GADI_WAVES")));
   if (getenv("GADI_MIN_CHUNK")) c->min_chunk = std::max(1, atoi(getenv("GADI_MIN_CHUNK")));
+  if (getenv("GADI_LOCKSTEP")) c->lockstep = atoi(getenv("GADI_LOCKSTEP"));
   if (c->kind == GADI_STENCIL) {
     c->nx = (int)desc->dims[0];
     c->ny = (int)desc->dims[1];

@@ -65,6 +65,58 @@ __device__ __forceinline__ CT madd(CT c, CT v, CT acc) {
   return fma_rn(c, v, acc);
 }
 
+// ------------------------------------------------------------ packed fp32x2
+// Blackwell executes fp32 add/mul/fma on register pairs (SASS FFMA2/FADD2/
+// FMUL2): half the instruction count of the scalar forms for the
+// storage-model arithmetic.  Pairs are (element 2j, element 2j+1).
+__device__ __forceinline__ unsigned long long f2u(float2 a) {
+  unsigned long long u;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(u) : "f"(a.x), "f"(a.y));
+  return u;
+}
+__device__ __forceinline__ float2 u2f(unsigned long long u) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(u));
+  return a;
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 bcast2(float a) { return make_float2(a, a); }
+
+// bf16x2 word -> two floats with one integer op each (bf16 is the top half
+// of an fp32 pattern): lo = w << 16, hi = w & 0xffff0000.
+__device__ __forceinline__ float bf_lo(unsigned w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(unsigned w) { return __uint_as_float(w & 0xffff0000u); }
+
+// RNE-round a pair of floats onto the storage grid (packed conversion for
+// bf16/fp16: one F2FP per pair) and return the rounded values as floats.
+template <class ST>
+__device__ __forceinline__ float2 round2(float2 v) {
+  if constexpr (std::is_same<ST, bf16>::value) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
+    const unsigned w = *reinterpret_cast<const unsigned*>(&h);
+    return make_float2(bf_lo(w), bf_hi(w));
+  } else if constexpr (std::is_same<ST, fp16>::value) {
+    const __half2 h = __floats2half2_rn(v.x, v.y);
+    return __half22float2(h);
+  } else {
+    return v;
+  }
+}
+
 // ------------------------------------------------------------ vector memory
 // Load VZ consecutive elements (element index idx, VZ-aligned when VEC) and
 // convert to the compute type. Read-only arrays go through the non-coherent
@@ -73,7 +125,18 @@ template <class T, int VZ, bool NC, class CT>
 __device__ __forceinline__ void load_vec(const T* __restrict__ p, long long idx, CT (&out)[VZ]) {
   constexpr int BYTES = VZ * (int)sizeof(T);
   const T* q = p + idx;
-  if constexpr (BYTES % 16 == 0) {
+  if constexpr (std::is_same<T, bf16>::value && std::is_same<CT, float>::value && BYTES % 16 == 0) {
+#pragma unroll
+    for (int c = 0; c < BYTES / 16; ++c) {
+      const uint4 u = NC ? __ldg(reinterpret_cast<const uint4*>(q) + c) : __ldcg(reinterpret_cast<const uint4*>(q) + c);
+      const unsigned w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        out[c * 8 + 2 * j] = bf_lo(w[j]);
+        out[c * 8 + 2 * j + 1] = bf_hi(w[j]);
+      }
+    }
+  } else if constexpr (BYTES % 16 == 0) {
     constexpr int PER = 16 / (int)sizeof(T);
 #pragma unroll
     for (int c = 0; c < BYTES / 16; ++c) {
@@ -125,8 +188,17 @@ __device__ __forceinline__ void store_any(T* __restrict__ p, long long idx, int 
                                           bool vec) {
   constexpr int BYTES = VZ * (int)sizeof(T);
   T tmp[VZ];
+  if constexpr (std::is_same<CT, float>::value && std::is_same<T, bf16>::value && VZ % 2 == 0) {
 #pragma unroll
-  for (int j = 0; j < VZ; ++j) tmp[j] = Store<T>::from(v[j]);
+    for (int j = 0; j < VZ; j += 2)
+      *reinterpret_cast<__nv_bfloat162*>(&tmp[j]) = __floats2bfloat162_rn(v[j], v[j + 1]);
+  } else if constexpr (std::is_same<CT, float>::value && std::is_same<T, fp16>::value && VZ % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < VZ; j += 2) *reinterpret_cast<__half2*>(&tmp[j]) = __floats2half2_rn(v[j], v[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < VZ; ++j) tmp[j] = Store<T>::from(v[j]);
+  }
   if (vec && nvalid >= VZ) {
     if constexpr (BYTES % 16 == 0) {
 #pragma unroll

@@ -70,6 +70,7 @@ struct Ctx {
   int no_tma = 0;  // force the register-prefetch sweep (testing)
   int waves = 1;      // grid size in waves of resident CTAs (TMA sweep)
   int min_chunk = 8;  // lower bound on planes per CTA
+  int lockstep = 0;   // TMA sweep: align x-chunks across tiles (L2 halo reuse; slower on B200)
   double last_norm_ms = 0.0;
 
   // live per-kernel timers: event pairs around every launch while enabled,

@@ -33,18 +33,31 @@ inline int launch_sweep(Ctx* c, P& p) {
   p.partials = c->partials;
   p.ticket = c->ticket;
   if (tma_aligned<P>(c)) {
+    // one resident wave of CTAs; the kernel splits the (tile, plane) units
+    // evenly among them (SegIter)
     const size_t smem = TmaShape<P>::SMEM;
+    constexpr int NTH = TmaThreads<P>::NTOT;
     static int occ = 0;
     if (!occ) {
       GADI_CUDA(cudaFuncSetAttribute(sweep_tma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma_kernel<P>, P::NT + 32, smem));
+      GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma_kernel<P>, NTH, smem));
       if (occ < 1) occ = 1;
     }
     p.g = make_geom(c, S::TZ, S::TY, P::VZ, (long long)occ * c->sms);
-    const int nb = geom_blocks(p.g);
+    const long long tiles = (long long)p.g.nzt * p.g.nyt;
+    const long long units = tiles * p.g.nx;
+    const long long slots = (long long)occ * c->sms * c->waves;
+    long long nbl = std::min(units, slots);
+    if (c->lockstep && tiles <= slots) {
+      // every tile split into the same k x-chunks: CTAs on neighbouring tiles
+      // sweep the same planes at the same time, so y-halo rows hit in L2
+      const long long k = std::max(1LL, std::min(slots / tiles, (long long)p.g.nx / std::max(1, c->min_chunk)));
+      nbl = tiles * k;
+    }
+    const int nb = (int)nbl;
     if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
     prof_begin(c, P::KID);
-    sweep_tma_kernel<P><<<nb, P::NT + 32, smem, c->stream>>>(p);
+    sweep_tma_kernel<P><<<nb, NTH, smem, c->stream>>>(p);
     prof_end(c);
   } else {
     p.g = make_geom(c, S::TZ, S::TY, P::VZ);
@@ -124,13 +137,23 @@ struct Engine {
       const int nb = std::min(batch, maxit - launched);
       for (int j = 0; j < nb; ++j) {
         const int k = launched + j;
-        HcgA<G> a;
-        a.st = c->hst;
-        a.r = (const ST*)c->R;
-        a.pin = P[k & 1];
-        a.pout = P[(k + 1) & 1];
-        a.H = H;
-        GADI_TRY(launch_sweep(c, a));
+        if (k == 0) {
+          HcgA<G, true> a;
+          a.st = c->hst;
+          a.r = (const ST*)c->R;
+          a.pin = P[0];
+          a.pout = P[1];
+          a.H = H;
+          GADI_TRY(launch_sweep(c, a));
+        } else {
+          HcgA<G> a;
+          a.st = c->hst;
+          a.r = (const ST*)c->R;
+          a.pin = P[k & 1];
+          a.pout = P[(k + 1) & 1];
+          a.H = H;
+          GADI_TRY(launch_sweep(c, a));
+        }
         HcgB<G> b;
         b.st = c->hst;
         b.p = P[(k + 1) & 1];
@@ -174,13 +197,23 @@ struct Engine {
       const int nb = std::min(batch, maxit - launched);
       for (int j = 0; j < nb; ++j) {
         const int k = launched + j;
-        CgnrP1<G> p1;
-        p1.st = c->sst;
-        p1.rbar = (const ST*)c->RB;
-        p1.pin = P[k & 1];
-        p1.pout = P[(k + 1) & 1];
-        p1.S = S;
-        GADI_TRY(launch_sweep(c, p1));
+        if (k == 0) {
+          CgnrP1<G, true> p1;
+          p1.st = c->sst;
+          p1.rbar = (const ST*)c->RB;
+          p1.pin = P[0];
+          p1.pout = P[1];
+          p1.S = S;
+          GADI_TRY(launch_sweep(c, p1));
+        } else {
+          CgnrP1<G> p1;
+          p1.st = c->sst;
+          p1.rbar = (const ST*)c->RB;
+          p1.pin = P[k & 1];
+          p1.pout = P[(k + 1) & 1];
+          p1.S = S;
+          GADI_TRY(launch_sweep(c, p1));
+        }
         CgnrP2<G> p2;
         p2.st = c->sst;
         p2.p = P[(k + 1) & 1];

@@ -38,6 +38,10 @@ struct GeoT {
   static constexpr int BY = DIM == 3 ? 8 : 1;
   static constexpr int ZS = ZS_;
   static constexpr int NT = BZ * BY;
+#ifndef GADI_TMA_MINB
+#define GADI_TMA_MINB 2
+#endif
+  static constexpr int MINB = GADI_TMA_MINB;  // CTAs per SM the TMA sweep is register-budgeted for
 };
 
 // Kernel ids for the live per-kernel timers (gadi_prof_*).
@@ -66,10 +70,64 @@ struct NormState {
 template <class CT, int VZ>
 __device__ __forceinline__ double dotv(const CT (&a)[VZ], const CT (&b)[VZ], int nv) {
   CT acc = CT(0);
+  if (nv == VZ) {
+    if constexpr (std::is_same<CT, float>::value && VZ % 2 == 0) {
+      float2 a2 = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int k = 0; k < VZ; ++k)
-    if (k < nv) acc = fma_rn(a[k], b[k], acc);
+      for (int k = 0; k < VZ; k += 2) a2 = ffma2(make_float2(a[k], a[k + 1]), make_float2(b[k], b[k + 1]), a2);
+      return (double)(a2.x + a2.y);
+    }
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) acc = fma_rn(a[k], b[k], acc);
+  } else {
+#pragma unroll
+    for (int k = 0; k < VZ; ++k)
+      if (k < nv) acc = fma_rn(a[k], b[k], acc);
+  }
   return (double)acc;
+}
+
+// Per-vector stencil for the storage model: packed fp32x2 when the compute
+// type is float, element-wise ordered arithmetic otherwise (fp64 storage).
+template <bool ORD, bool HASY, int VZ, int ZS, class CT>
+__device__ __forceinline__ void stencil_vec_any(const CoefT<CT>& c, const CT (&xm)[VZ], const CT (&ym)[VZ],
+                                                const CT (&ce)[VZ], const CT (&lf)[ZS], const CT (&rt)[ZS],
+                                                const CT (&yp)[VZ], const CT (&xp)[VZ], CT (&out)[VZ]) {
+  if constexpr (std::is_same<CT, float>::value && !ORD && VZ % 2 == 0) {
+    stencil_packed<HASY, VZ, ZS>(c, xm, ym, ce, lf, rt, yp, xp, out);
+  } else {
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) {
+      const CT zm = (k >= ZS) ? ce[k - ZS] : lf[k];
+      const CT zp = (k + ZS < VZ) ? ce[k + ZS] : rt[k + ZS - VZ];
+      out[k] = apply_stencil<ORD>(c, CT(0), xm[k], ym[k], zm, ce[k], zp, yp[k], xp[k]);
+    }
+  }
+}
+
+#define GADI_STENCIL_VEC(COEF)                                                                              \
+  __device__ void stencil_vec(int, const CT (&xm)[G::VZ], const CT (&ym)[G::VZ], const CT (&ce)[G::VZ],     \
+                              const CT (&lf)[G::ZS], const CT (&rt)[G::ZS], const CT (&yp)[G::VZ],          \
+                              const CT (&xp)[G::VZ], CT (&out)[G::VZ]) const {                              \
+    stencil_vec_any<ORD, (G::BY > 1), G::VZ, G::ZS>(COEF, xm, ym, ce, lf, rt, yp, xp, out);                  \
+  }
+
+// y[k] = round(c + s * a[k]) (axpy rounded to storage) on a whole vector,
+// packed fp32x2 when possible
+template <class ST, int VZ, class CT>
+__device__ __forceinline__ void axpy_round(CT s, const CT (&a)[VZ], const CT (&c)[VZ], CT (&y)[VZ]) {
+  if constexpr (std::is_same<CT, float>::value && VZ % 2 == 0) {
+    const float2 s2 = bcast2(s);
+#pragma unroll
+    for (int k = 0; k < VZ; k += 2) {
+      const float2 v = round2<ST>(ffma2(s2, make_float2(a[k], a[k + 1]), make_float2(c[k], c[k + 1])));
+      y[k] = v.x;
+      y[k + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) y[k] = round_to<ST>(fma_rn(s, a[k], c[k]));
+  }
 }
 
 // Common plumbing every pass carries.
@@ -81,7 +139,7 @@ struct PassBase {
 
 // ============================================================== H-CG passes
 // f = (it == 0) ? r : round(r + beta p_in) ; Hf ; store p_out ; sum f.Hf
-template <class G>
+template <class G, bool FIRST = false>
 struct HcgA : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
@@ -95,16 +153,24 @@ struct HcgA : G, PassBase {
   ST* pout;
   CoefT<CT> H;
   CT beta;
-  bool first;
+  static constexpr bool first = FIRST;  // iteration 0: p = r, p_in is not read
   struct Raw { CT r[G::VZ], p[G::VZ]; };
   struct RawS { CT r, p; };
   struct Epi {};
   __device__ bool prepare() {
     if (st->done) return false;
-    first = (st->it == 0);
     beta = (CT)st->beta;
     return true;
   }
+  __device__ void field_vec(const Raw& a, CT (&f)[1][G::VZ]) const {
+    if constexpr (FIRST) {
+#pragma unroll
+      for (int k = 0; k < G::VZ; ++k) f[0][k] = a.r[k];
+    } else {
+      axpy_round<ST>(beta, a.p, a.r, f[0]);
+    }
+  }
+  GADI_STENCIL_VEC(H)
   static constexpr int NIN = 2, NE = 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return 1; }
@@ -174,6 +240,7 @@ struct HcgB : G, PassBase {
     alpha = (CT)st->alpha;
     return true;
   }
+  GADI_STENCIL_VEC(H)
   static constexpr int NIN = 1, NE = 2;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return (int)sizeof(ST); }
@@ -200,11 +267,8 @@ struct HcgB : G, PassBase {
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
                            double (&red)[1]) const {
     CT zn[G::VZ], rn[G::VZ];
-#pragma unroll
-    for (int k = 0; k < G::VZ; ++k) {
-      zn[k] = round_to<ST>(fma_rn(alpha, fc[0][k], e.z[k]));
-      rn[k] = round_to<ST>(fma_rn(-alpha, s[0][k], e.r[k]));
-    }
+    axpy_round<ST>(alpha, fc[0], e.z, zn);
+    axpy_round<ST>(-alpha, s[0], e.r, rn);
     red[0] += dotv<CT, G::VZ>(rn, rn, nv);
     store_any<ST, G::VZ>(z, i, nv, zn, g.vec);
     store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
@@ -253,6 +317,7 @@ struct CgnrInit : G, PassBase {
   struct RawS { CT z; };
   struct Epi {};
   __device__ bool prepare() { return true; }
+  GADI_STENCIL_VEC(ST_)
   static constexpr int NIN = 1, NE = 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return 1; }
@@ -309,7 +374,7 @@ struct CgnrInit : G, PassBase {
 };
 
 // f = (it==0) ? rbar : round(rbar + beta p_in) ; w = S f ; store p_out ; sum w.w
-template <class G>
+template <class G, bool FIRST = false>
 struct CgnrP1 : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
@@ -323,16 +388,24 @@ struct CgnrP1 : G, PassBase {
   ST* pout;
   CoefT<CT> S;
   CT beta;
-  bool first;
+  static constexpr bool first = FIRST;
   struct Raw { CT rb[G::VZ], p[G::VZ]; };
   struct RawS { CT rb, p; };
   struct Epi {};
   __device__ bool prepare() {
     if (st->done) return false;
-    first = (st->it == 0);
     beta = (CT)st->beta;
     return true;
   }
+  __device__ void field_vec(const Raw& a, CT (&f)[1][G::VZ]) const {
+    if constexpr (FIRST) {
+#pragma unroll
+      for (int k = 0; k < G::VZ; ++k) f[0][k] = a.rb[k];
+    } else {
+      axpy_round<ST>(beta, a.p, a.rb, f[0]);
+    }
+  }
+  GADI_STENCIL_VEC(S)
   static constexpr int NIN = 2, NE = 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return 1; }
@@ -402,6 +475,7 @@ struct CgnrP2 : G, PassBase {
     alpha = (CT)st->alpha;
     return true;
   }
+  GADI_STENCIL_VEC(S)
   static constexpr int NIN = 1, NE = 2;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return (int)sizeof(ST); }
@@ -428,12 +502,11 @@ struct CgnrP2 : G, PassBase {
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
                            double (&red)[1]) const {
     CT yn[G::VZ], rn[G::VZ];
+    axpy_round<ST>(alpha, fc[0], e.y, yn);
+    axpy_round<ST>(-alpha, s[0], e.r, rn);
 #pragma unroll
-    for (int k = 0; k < G::VZ; ++k) {
-      yn[k] = round_to<ST>(fma_rn(alpha, fc[0][k], e.y[k]));
-      rn[k] = round_to<ST>(fma_rn(-alpha, s[0][k], e.r[k]));
+    for (int k = 0; k < G::VZ; ++k)
       if (k < nv) red[0] += (double)rn[k] * (double)rn[k];
-    }
     store_any<ST, G::VZ>(y, i, nv, yn, g.vec);
     store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
   }
@@ -468,6 +541,7 @@ struct CgnrP3 : G, PassBase {
   struct RawS { CT r; };
   struct Epi {};
   __device__ bool prepare() { return !st->done; }
+  GADI_STENCIL_VEC(ST_)
   static constexpr int NIN = 1, NE = 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return 1; }
@@ -525,6 +599,7 @@ struct Outer : G, PassBase {
   static constexpr int NF = 1 + (HAS_E ? 1 : 0) + (UR != 0 ? 1 : 0);
   static constexpr int FU = NF - 1;
   static constexpr int NR = 6;
+  static constexpr int MINB = 1;  // two fp64 fields: let ptxas keep them in registers
   static constexpr bool HAS_RED = true, ORD = true, TMA_OK = !CPLX;
   static constexpr int KID = K_OUTER;
   static __device__ __forceinline__ int op(int s) { return s == 1 ? RED_MAX : RED_SUM; }
@@ -681,13 +756,13 @@ struct NormPass : G, PassBase {
   double* outv;
   const double* v;  // crd potential
   CoefT<double> A;  // A (TRANS=false) or A^T (TRANS=true)
-  double nw;
+  double rnw;       // 1 / ||w||
   struct Raw { double a[VZ]; };
   struct RawS { double a; };
   struct Epi { double v[VZ]; };
   __device__ bool prepare() {
     if (ns->done) return false;
-    nw = ns->nw;
+    rnw = 1.0 / ns->nw;
     return true;
   }
   static constexpr int NIN = 1, NE = 0;
@@ -699,7 +774,10 @@ struct NormPass : G, PassBase {
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const { lds_vec<double, VZ>(R.p[0], z, a.a); }
   __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int z) const { a.a = lds1<double, double>(R.p[0], z); }
   __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
-  __device__ double fv(double a) const { return TRANS ? a : __ddiv_rn(a, nw); }  // analysis.py:66 v = w / nw
+  // analysis.py:66 v = w / nw, as a multiply by the reciprocal (one DMUL
+  // instead of a division sequence per element; differs from the division
+  // by at most one rounding, far below the power iteration's 1e-6 tolerance)
+  __device__ double fv(double a) const { return TRANS ? a : a * rnw; }
   __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<double, VZ, true>(in, i, nv, a.a, g.vec); }
   __device__ void load_raw_s(RawS& a, long long i) const { a.a = in[i]; }
   __device__ void field(const Raw& a, int k, double (&f)[1]) const { f[0] = fv(a.a[k]); }

@@ -55,6 +55,17 @@ template <class CT> struct CoefT {
 template <bool ORD, class CT>
 __device__ __forceinline__ CT apply_stencil(const CoefT<CT>& c, CT acc, CT xm, CT ym, CT zm, CT ce, CT zp, CT yp,
                                             CT xp) {
+  if constexpr (!ORD) {
+    // storage model: a zero coefficient contributes an exact 0 (finite
+    // operands), so the fused chain needs no presence tests
+    acc = fma_rn(c.lo[0], xm, acc);
+    acc = fma_rn(c.lo[1], ym, acc);
+    acc = fma_rn(c.lo[2], zm, acc);
+    acc = fma_rn(c.d, ce, acc);
+    acc = fma_rn(c.up[2], zp, acc);
+    acc = fma_rn(c.up[1], yp, acc);
+    return fma_rn(c.up[0], xp, acc);
+  }
   if (c.lo[0] != CT(0)) acc = madd<ORD>(c.lo[0], xm, acc);
   if (c.lo[1] != CT(0)) acc = madd<ORD>(c.lo[1], ym, acc);
   if (c.lo[2] != CT(0)) acc = madd<ORD>(c.lo[2], zm, acc);
@@ -63,6 +74,41 @@ __device__ __forceinline__ CT apply_stencil(const CoefT<CT>& c, CT acc, CT xm, C
   if (c.up[1] != CT(0)) acc = madd<ORD>(c.up[1], yp, acc);
   if (c.up[0] != CT(0)) acc = madd<ORD>(c.up[0], xp, acc);
   return acc;
+}
+
+// Optional per-vector hooks: a pass may process a lane's whole VZ-vector at
+// once (packed fp32x2 arithmetic) instead of element by element.
+template <class P, class = void> struct HasStencilVec : std::false_type {};
+template <class P> struct HasStencilVec<P, std::void_t<decltype(&P::stencil_vec)>> : std::true_type {};
+template <class P, class = void> struct HasFieldVec : std::false_type {};
+template <class P> struct HasFieldVec<P, std::void_t<decltype(&P::field_vec)>> : std::true_type {};
+
+// Storage-model 7-point stencil on a lane's vector with packed fp32x2 FMAs
+// for the x, y and centre terms (pairs of adjacent z-elements) and scalar
+// FMAs for the z-neighbours (which straddle pairs).  HASY = 3-D.
+template <bool HASY, int VZ, int ZS>
+__device__ __forceinline__ void stencil_packed(const CoefT<float>& c, const float (&xm)[VZ], const float (&ym)[VZ],
+                                               const float (&ce)[VZ], const float (&left)[ZS],
+                                               const float (&right)[ZS], const float (&yp)[VZ],
+                                               const float (&xp)[VZ], float (&out)[VZ]) {
+  const float2 clx = bcast2(c.lo[0]), cd = bcast2(c.d), cux = bcast2(c.up[0]);
+  const float2 cly = bcast2(c.lo[1]), cuy = bcast2(c.up[1]);
+#pragma unroll
+  for (int j = 0; j < VZ; j += 2) {
+    float2 acc = fmul2(cd, make_float2(ce[j], ce[j + 1]));
+    acc = ffma2(clx, make_float2(xm[j], xm[j + 1]), acc);
+    acc = ffma2(cux, make_float2(xp[j], xp[j + 1]), acc);
+    if constexpr (HASY) {
+      acc = ffma2(cly, make_float2(ym[j], ym[j + 1]), acc);
+      acc = ffma2(cuy, make_float2(yp[j], yp[j + 1]), acc);
+    }
+    const float zm0 = (j >= ZS) ? ce[j - ZS] : left[j];
+    const float zm1 = (j + 1 >= ZS) ? ce[j + 1 - ZS] : left[j + 1];
+    const float zp0 = (j + ZS < VZ) ? ce[j + ZS] : right[j + ZS - VZ];
+    const float zp1 = (j + 1 + ZS < VZ) ? ce[j + 1 + ZS] : right[j + 1 + ZS - VZ];
+    out[j] = fmaf(c.up[2], zp0, fmaf(c.lo[2], zm0, acc.x));
+    out[j + 1] = fmaf(c.up[2], zp1, fmaf(c.lo[2], zm1, acc.y));
+  }
 }
 
 // Tiling constants shared by a pass and its host launcher.
@@ -144,6 +190,12 @@ __global__ void __launch_bounds__(P::NT) sweep_kernel(P p) {
   };
 
   auto fields = [&](const typename P::Raw& raw, int nv, CT (&f)[NF][VZ]) {
+    if constexpr (HasFieldVec<P>::value) {
+      if (nv == VZ) {
+        p.field_vec(raw, f);
+        return;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < VZ; ++k) {
       CT t[NF];
@@ -262,12 +314,22 @@ __global__ void __launch_bounds__(P::NT) sweep_kernel(P p) {
         left[j] = (lane == 0) ? rowc[-ZS + j] : fromprev;
         right[j] = (lane == 31) ? rowc[VZ + j] : fromnext;
       }
+      if constexpr (HasStencilVec<P>::value) {
+        CT ym[VZ], yp[VZ];
 #pragma unroll
-      for (int k = 0; k < VZ; ++k) {
-        const CT zm = (k >= ZS) ? fcur[q][k - ZS] : left[k];
-        const CT zp = (k + ZS < VZ) ? fcur[q][k + ZS] : right[k + ZS - VZ];
-        const Nb<CT> nb{fprev[q][k], rowm[k], zm, fcur[q][k], zp, rowp[k], fnext[q][k]};
-        st[q][k] = p.stencil(q, k, nb, fcur, E);
+        for (int k = 0; k < VZ; ++k) {
+          ym[k] = rowm[k];
+          yp[k] = rowp[k];
+        }
+        p.stencil_vec(q, fprev[q], ym, fcur[q], left, right, yp, fnext[q], st[q]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) {
+          const CT zm = (k >= ZS) ? fcur[q][k - ZS] : left[k];
+          const CT zp = (k + ZS < VZ) ? fcur[q][k + ZS] : right[k + ZS - VZ];
+          const Nb<CT> nb{fprev[q][k], rowm[k], zm, fcur[q][k], zp, rowp[k], fnext[q][k]};
+          st[q][k] = p.stencil(q, k, nb, fcur, E);
+        }
       }
     }
     if (nvz > 0) p.epilogue(gidx(x, y, zb), nvz, fcur, st, E, red);

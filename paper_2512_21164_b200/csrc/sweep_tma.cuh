@@ -63,7 +63,18 @@ template <class T, int VZ, class CT>
 __device__ __forceinline__ void lds_vec(const unsigned char* row, int zoff, CT (&out)[VZ]) {
   const T* q = reinterpret_cast<const T*>(row) + zoff;
   constexpr int BYTES = VZ * (int)sizeof(T);
-  if constexpr (BYTES % 16 == 0) {
+  if constexpr (std::is_same<T, bf16>::value && std::is_same<CT, float>::value && BYTES % 16 == 0) {
+#pragma unroll
+    for (int c = 0; c < BYTES / 16; ++c) {
+      const uint4 u = reinterpret_cast<const uint4*>(q)[c];
+      const unsigned w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        out[c * 8 + 2 * j] = bf_lo(w[j]);
+        out[c * 8 + 2 * j + 1] = bf_hi(w[j]);
+      }
+    }
+  } else if constexpr (BYTES % 16 == 0) {
     constexpr int PER = 16 / (int)sizeof(T);
 #pragma unroll
     for (int c = 0; c < BYTES / 16; ++c) {
@@ -110,21 +121,59 @@ template <class P> struct TmaShape {
   }
   static constexpr int STAGE = off_epi(P::NE);
   static constexpr int FBYTES = (int)B::SMEM;  // two f-plane buffers
-  static constexpr int BUDGET = 110 * 1024;
+#ifndef GADI_TMA_BUDGET_KB
+#define GADI_TMA_BUDGET_KB 110
+#endif
+  static constexpr int BUDGET = GADI_TMA_BUDGET_KB * 1024;
   static constexpr int NST_RAW = (BUDGET - FBYTES) / STAGE;
   static constexpr int NST = NST_RAW < 2 ? 2 : (NST_RAW > 8 ? 8 : NST_RAW);
   static constexpr size_t SMEM = (size_t)FBYTES + (size_t)NST * STAGE + 2 * NST * sizeof(uint64_t);
 };
 
+// Threads: NT compute threads (BZ x BY), NH halo warps (3-D: one per y-halo
+// row, so the compute warps stay balanced), one producer warp.
+template <class P> struct TmaThreads {
+  static constexpr int NH = P::BY > 1 ? 2 : 0;
+  static constexpr int NCONS = P::NT + 32 * NH;  // consumer threads
+  static constexpr int NTOT = NCONS + 32;
+};
+
+// Work decomposition: the (tile, x-plane) units are split into gridDim.x
+// equal contiguous ranges (one CTA per resident slot, a single wave); a
+// range is a list of x-segments of at most a few tiles.  Every segment
+// re-primes the register queue from planes xa-1, xa; the stage ring and the
+// mbarrier phases run on across segments.
+struct SegIter {
+  long long u, u1;
+  int nx, tiles;
+  __device__ SegIter(const SweepGeom& g, int nblocks, int b) {
+    nx = g.nx;
+    tiles = g.nzt * g.nyt;
+    const long long T = (long long)tiles * nx;
+    const long long W = (T + nblocks - 1) / nblocks;
+    u = (long long)b * W;
+    u1 = min(T, u + W);
+  }
+  __device__ bool next(int& tile, int& xa, int& xb) {
+    if (u >= u1) return false;
+    tile = (int)(u / nx);
+    xa = (int)(u % nx);
+    xb = (int)min((long long)nx, xa + (u1 - u));
+    u += xb - xa;
+    return true;
+  }
+};
+
 template <class P>
-__global__ void __launch_bounds__(P::NT + 32) sweep_tma_kernel(P p) {
+__global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel(P p) {
   using S = SweepShape<P>;
   using TS = TmaShape<P>;
+  using TH = TmaThreads<P>;
   using CT = typename P::CT;
   constexpr int VZ = S::VZ, BZ = S::BZ, BY = S::BY, ZS = S::ZS, NF = S::NF;
   constexpr int TZ = S::TZ, TY = S::TY, PAD = S::PAD, ROW = S::ROW;
   constexpr int NR = P::NR, NT = P::NT, NIN = P::NIN, NE = P::NE, NST = TS::NST;
-  constexpr int NWC = NT / 32;  // consumer warps
+  constexpr int NCONS = TH::NCONS, NWCONS = NCONS / 32;
   static_assert(NIN <= 4 && NE <= 4, "at most four inputs of each kind");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   CT* fsm = reinterpret_cast<CT*>(smem_raw);
@@ -136,20 +185,12 @@ __global__ void __launch_bounds__(P::NT + 32) sweep_tma_kernel(P p) {
 
   const SweepGeom g = p.g;
   const int tid = threadIdx.x;
-  int bidx = blockIdx.x;
-  const int ztile = bidx % g.nzt;
-  bidx /= g.nzt;
-  const int ytile = bidx % g.nyt;
-  bidx /= g.nyt;
-  const int xa = bidx * g.xchunk;
-  const int xb = min(g.nx, xa + g.xchunk);
-  const int zt0 = ztile * TZ, y0 = ytile * TY;
-  const int nplanes = xb - xa + 2;  // xa-1 .. xb
+  const int lane = tid & 31;
 
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWC);
+      mbar_init(&empty[s], NWCONS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -159,74 +200,73 @@ __global__ void __launch_bounds__(P::NT + 32) sweep_tma_kernel(P p) {
 #pragma unroll
   for (int s = 0; s < NR; ++s) red[s] = 0.0;
 
-  if (tid >= NT) {
+  if (tid >= NCONS) {
     // ------------------------------------------------------------ producer
     // the whole warp issues the row copies of a stage (one row per lane),
     // lane 0 posts the byte count first
-    const int lane = tid & 31;
     constexpr int NCOPY = NIN * (TY + 2) + NE * TY;
-    for (int s = 0; s < nplanes; ++s) {
-      const int xp = xa - 1 + s;
-      const int st = s % NST;
-      if (s >= NST) mbar_wait(&empty[st], (unsigned)(((s / NST) - 1) & 1));
-      unsigned char* sb = stages + (size_t)st * TS::STAGE;
-      const bool pv = (xp >= 0 && xp < g.nx);
-      const bool ev = pv && xp >= xa && xp < xb;
-      unsigned bytes = 0;
-      if (pv) {
+    SegIter it(g, gridDim.x, blockIdx.x);
+    int tile, xa, xb;
+    int gs = 0;
+    while (it.next(tile, xa, xb)) {
+      const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+      for (int xp = xa - 1; xp <= xb; ++xp, ++gs) {
+        const int st = gs % NST;
+        if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
+        unsigned char* sb = stages + (size_t)st * TS::STAGE;
+        const bool pv = (xp >= 0 && xp < g.nx);
+        const bool ev = pv && xp >= xa && xp < xb;
+        unsigned bytes = 0;
+        if (pv) {
 #pragma unroll
-        for (int j = 0; j < NIN; ++j)
-          if (p.in_active(j))
-            for (int r = 0; r < TY + 2; ++r) {
-              const int yy = y0 - 1 + r;
-              if (yy >= 0 && yy < g.ny) bytes += TS::rb_in(j);
-            }
-        if (ev) {
+          for (int j = 0; j < NIN; ++j)
+            if (p.in_active(j))
+              for (int r = 0; r < TY + 2; ++r) {
+                const int yy = y0 - 1 + r;
+                if (yy >= 0 && yy < g.ny) bytes += TS::rb_in(j);
+              }
+          if (ev) {
 #pragma unroll
-          for (int j = 0; j < NE; ++j)
-            for (int r = 0; r < TY; ++r)
-              if (y0 + r < g.ny) bytes += TS::rb_epi(j);
+            for (int j = 0; j < NE; ++j)
+              for (int r = 0; r < TY; ++r)
+                if (y0 + r < g.ny) bytes += TS::rb_epi(j);
+          }
         }
-      }
-      if (lane == 0) mbar_expect_tx(&full[st], bytes);
-      __syncwarp();
-      if (pv) {
-        for (int q = lane; q < NCOPY; q += 32) {
-          if (q < NIN * (TY + 2)) {
-            const int j = q / (TY + 2), r = q % (TY + 2);
-            const int yy = y0 - 1 + r;
-            if (!p.in_active(j) || yy < 0 || yy >= g.ny) continue;
-            const int esz = P::in_esz(j), hz = TS::hz(esz);
-            const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
-            const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0 - hz;
-            bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j), base + e0 * esz, (unsigned)TS::rb_in(j), &full[st]);
-          } else if (ev) {
-            const int q2 = q - NIN * (TY + 2);
-            const int j = q2 / TY, r = q2 % TY;
-            const int yy = y0 + r;
-            if (yy >= g.ny) continue;
-            const int esz = P::epi_esz(j);
-            const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
-            const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0;
-            bulk_g2s(sb + TS::off_epi(j) + r * TS::rb_epi(j), base + e0 * esz, (unsigned)TS::rb_epi(j), &full[st]);
+        if (lane == 0) mbar_expect_tx(&full[st], bytes);
+        __syncwarp();
+        if (pv) {
+          for (int q = lane; q < NCOPY; q += 32) {
+            if (q < NIN * (TY + 2)) {
+              const int j = q / (TY + 2), r = q % (TY + 2);
+              const int yy = y0 - 1 + r;
+              if (!p.in_active(j) || yy < 0 || yy >= g.ny) continue;
+              const int esz = P::in_esz(j), hz = TS::hz(esz);
+              const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
+              const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0 - hz;
+              bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j), base + e0 * esz, (unsigned)TS::rb_in(j), &full[st]);
+            } else if (ev) {
+              const int q2 = q - NIN * (TY + 2);
+              const int j = q2 / TY, r = q2 % TY;
+              const int yy = y0 + r;
+              if (yy >= g.ny) continue;
+              const int esz = P::epi_esz(j);
+              const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
+              const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0;
+              bulk_g2s(sb + TS::off_epi(j) + r * TS::rb_epi(j), base + e0 * esz, (unsigned)TS::rb_epi(j),
+                       &full[st]);
+            }
           }
         }
       }
     }
   } else {
     // ------------------------------------------------------------ consumers
-    const int tz = tid % BZ, ty = tid / BZ, lane = tid & 31;
-    const int zb = zt0 + tz * VZ, y = y0 + ty;
-    const bool yok = y < g.ny;
-    const int nvz = yok ? max(0, min(VZ, g.nz - zb)) : 0;
-    const bool own_hm = (ty == 0), own_hp = (ty == BY - 1);
-    const bool hm_ok = own_hm && y0 - 1 >= 0, hp_ok = own_hp && y0 + TY < g.ny;
-    const int nvh = max(0, min(VZ, g.nz - zb));
-    const bool own_zl = (tz == 0), own_zr = (tz == BZ - 1);
+    const bool halo_warp = tid >= NT;  // 3-D only: warp NT/32 -> row y0-1, NT/32+1 -> row y0+TY
+    const int hrow = halo_warp ? ((tid - NT) / 32 == 0 ? 0 : TY + 1) : 0;
+    const int tz = halo_warp ? lane : tid % BZ;
+    const int ty = halo_warp ? 0 : tid / BZ;
+    const bool own_zl = !halo_warp && (tz == 0), own_zr = !halo_warp && (tz == BZ - 1);
 
-    auto gidx = [&](int xx, int yy, int zz) -> long long {
-      return (long long)xx * g.plane + (long long)yy * g.nz + zz;
-    };
     // row r (0 .. TY+1, 0 = y0-1) of stage st, pointing at core element 0
     auto in_row = [&](int st, int r) {
       SmRow R;
@@ -247,75 +287,65 @@ __global__ void __launch_bounds__(P::NT + 32) sweep_tma_kernel(P p) {
       for (int j = 0; j < NE; ++j) R.p[j] = sb + TS::off_epi(j) + r * TS::rb_epi(j);
       return R;
     };
+    // nz % VZ == 0 on this path: a lane's vector is entirely valid or not
     auto fields_core = [&](int st, int r, int nv, CT (&f)[NF][VZ]) {
-      typename P::Raw a;
-      if (nv > 0) p.load_raw_sm(a, in_row(st, r), tz * VZ);
-#pragma unroll
-      for (int k = 0; k < VZ; ++k) {
-        CT t[NF];
-        if (k < nv) {
-          p.field(a, k, t);
+      if (nv == VZ) {
+        typename P::Raw a;
+        p.load_raw_sm(a, in_row(st, r), tz * VZ);
+        if constexpr (HasFieldVec<P>::value) {
+          p.field_vec(a, f);
         } else {
 #pragma unroll
-          for (int q = 0; q < NF; ++q) t[q] = CT(0);
-        }
+          for (int k = 0; k < VZ; ++k) {
+            CT t[NF];
+            p.field(a, k, t);
 #pragma unroll
-        for (int q = 0; q < NF; ++q) f[q][k] = t[q];
+            for (int q = 0; q < NF; ++q) f[q][k] = t[q];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < VZ; ++k)
+#pragma unroll
+          for (int q = 0; q < NF; ++q) f[q][k] = CT(0);
       }
     };
-    // the full f-plane (core, y-halo rows, z-halo) of the plane held by stage st
-    auto write_fplane = [&](CT* buf, int st, bool pv, const CT (&fc)[NF][VZ]) {
+    auto store_row = [&](CT* buf, int rr, const CT (&fc)[NF][VZ]) {
 #pragma unroll
       for (int q = 0; q < NF; ++q) {
-        CT* rowc = buf + ((size_t)q * (TY + 2) + (ty + 1)) * ROW + PAD + tz * VZ;
+        CT* row = buf + ((size_t)q * (TY + 2) + rr) * ROW + PAD + tz * VZ;
 #pragma unroll
-        for (int k = 0; k < VZ; ++k) rowc[k] = fc[q][k];
+        for (int k = 0; k < VZ; ++k) row[k] = fc[q][k];
       }
-      if (own_hm || own_hp) {
+    };
+    // z-halo scalars of this thread's row (edge lanes only)
+    auto store_zhalo = [&](CT* buf, int st, bool ok, int zt0) {
+      const SmRow R = in_row(st, ty + 1);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const bool mine = h == 0 ? own_hm : own_hp;
-          if (!mine) continue;
-          const bool ok = pv && (h == 0 ? hm_ok : hp_ok);
-          CT fh[NF][VZ];
-          fields_core(st, h == 0 ? 0 : TY + 1, ok ? nvh : 0, fh);
-          const int rr = h == 0 ? 0 : TY + 1;
+      for (int j = 0; j < ZS; ++j) {
+        const int zl = zt0 - ZS + j, zr = zt0 + TZ + j;
+        CT tl[NF], tr[NF];
+        if (own_zl && ok && zl >= 0) {
+          typename P::RawS a;
+          p.load_raw_s_sm(a, R, -ZS + j);
+          p.field_s(a, tl);
+        } else {
 #pragma unroll
-          for (int q = 0; q < NF; ++q) {
-            CT* row = buf + ((size_t)q * (TY + 2) + rr) * ROW + PAD + tz * VZ;
-#pragma unroll
-            for (int k = 0; k < VZ; ++k) row[k] = fh[q][k];
-          }
+          for (int q = 0; q < NF; ++q) tl[q] = CT(0);
         }
-      }
-      if (own_zl || own_zr) {
-        const SmRow R = in_row(st, ty + 1);
+        if (own_zr && ok && zr < g.nz) {
+          typename P::RawS a;
+          p.load_raw_s_sm(a, R, TZ + j);
+          p.field_s(a, tr);
+        } else {
 #pragma unroll
-        for (int j = 0; j < ZS; ++j) {
-          const int zl = zt0 - ZS + j, zr = zt0 + TZ + j;
-          CT tl[NF], tr[NF];
-          if (own_zl && pv && yok && zl >= 0) {
-            typename P::RawS a;
-            p.load_raw_s_sm(a, R, -ZS + j);
-            p.field_s(a, tl);
-          } else {
+          for (int q = 0; q < NF; ++q) tr[q] = CT(0);
+        }
 #pragma unroll
-            for (int q = 0; q < NF; ++q) tl[q] = CT(0);
-          }
-          if (own_zr && pv && yok && zr < g.nz) {
-            typename P::RawS a;
-            p.load_raw_s_sm(a, R, TZ + j);
-            p.field_s(a, tr);
-          } else {
-#pragma unroll
-            for (int q = 0; q < NF; ++q) tr[q] = CT(0);
-          }
-#pragma unroll
-          for (int q = 0; q < NF; ++q) {
-            CT* row = buf + ((size_t)q * (TY + 2) + (ty + 1)) * ROW;
-            if (own_zl) row[PAD - ZS + j] = tl[q];
-            if (own_zr) row[PAD + TZ + j] = tr[q];
-          }
+        for (int q = 0; q < NF; ++q) {
+          CT* row = buf + ((size_t)q * (TY + 2) + (ty + 1)) * ROW;
+          if (own_zl) row[PAD - ZS + j] = tl[q];
+          if (own_zr) row[PAD + TZ + j] = tr[q];
         }
       }
     };
@@ -323,71 +353,120 @@ __global__ void __launch_bounds__(P::NT + 32) sweep_tma_kernel(P p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s % NST]);
     };
+    auto wait_full = [&](int s) { mbar_wait(&full[s % NST], (unsigned)((s / NST) & 1)); };
 
-    CT fprev[NF][VZ], fcur[NF][VZ], fnext[NF][VZ];
-    // prologue: plane xa-1 (core only), plane xa (f-plane buffer 0)
-    {
-      mbar_wait(&full[0], 0u);
-      const bool pv = xa - 1 >= 0;
-      fields_core(0, ty + 1, pv ? nvz : 0, fprev);
-      release(0);
-      mbar_wait(&full[1 % NST], (unsigned)((1 / NST) & 1));
-      fields_core(1 % NST, ty + 1, nvz, fcur);
-      write_fplane(fsm, 1 % NST, true, fcur);
-    }
-    consumer_sync(NT);
-
-    for (int x = xa; x < xb; ++x) {
-      const int s = x - xa + 1;  // stage index of plane x
-      CT* bcur = fsm + (size_t)((x - xa) & 1) * S::PLANE;
-      CT* bnxt = fsm + (size_t)(((x - xa) + 1) & 1) * S::PLANE;
-      // 1. plane x+1 -> fnext + f-plane buffer
-      const int s1 = s + 1;
-      mbar_wait(&full[s1 % NST], (unsigned)((s1 / NST) & 1));
-      const bool pv1 = x + 1 < g.nx;
-      fields_core(s1 % NST, ty + 1, pv1 ? nvz : 0, fnext);
-      write_fplane(bnxt, s1 % NST, pv1, fnext);
-      // 2. stencil(s) and epilogue of plane x
-      typename P::Epi E;
-      p.load_epi_sm(E, epi_row(s % NST, ty), tz * VZ);
-      CT st[NF][VZ];
-#pragma unroll
-      for (int q = 0; q < NF; ++q) {
-        const CT* rowm = bcur + ((size_t)q * (TY + 2) + ty) * ROW + PAD + tz * VZ;
-        const CT* rowc = rowm + ROW;
-        const CT* rowp = rowc + ROW;
-        CT left[ZS], right[ZS];
-#pragma unroll
-        for (int j = 0; j < ZS; ++j) {
-          CT fromprev = __shfl_up_sync(0xffffffffu, fcur[q][VZ - ZS + j], 1);
-          CT fromnext = __shfl_down_sync(0xffffffffu, fcur[q][j], 1);
-          left[j] = (lane == 0) ? rowc[-ZS + j] : fromprev;
-          right[j] = (lane == 31) ? rowc[VZ + j] : fromnext;
-        }
-        CT ym[VZ], yp[VZ];
-#pragma unroll
-        for (int k = 0; k < VZ; ++k) {
-          ym[k] = rowm[k];
-          yp[k] = rowp[k];
-        }
-#pragma unroll
-        for (int k = 0; k < VZ; ++k) {
-          const CT zm = (k >= ZS) ? fcur[q][k - ZS] : left[k];
-          const CT zp = (k + ZS < VZ) ? fcur[q][k + ZS] : right[k + ZS - VZ];
-          const Nb<CT> nb{fprev[q][k], ym[k], zm, fcur[q][k], zp, yp[k], fnext[q][k]};
-          st[q][k] = p.stencil(q, k, nb, fcur, E);
-        }
+    if constexpr (TH::NH == 0) {
+      // 2-D: the y-halo rows of the f-plane buffers stay zero
+      for (int i = tid; i < 2 * NF * 2 * ROW; i += NCONS) {
+        const int buf = i / (NF * 2 * ROW), rem = i % (NF * 2 * ROW);
+        const int q = rem / (2 * ROW), rr = (rem / ROW) % 2 == 0 ? 0 : TY + 1, c = rem % ROW;
+        fsm[(size_t)buf * S::PLANE + ((size_t)q * (TY + 2) + rr) * ROW + c] = CT(0);
       }
-      if (nvz > 0) p.epilogue(gidx(x, y, zb), nvz, fcur, st, E, red);
-      release(s);
-#pragma unroll
-      for (int q = 0; q < NF; ++q)
-#pragma unroll
-        for (int k = 0; k < VZ; ++k) {
-          fprev[q][k] = fcur[q][k];
-          fcur[q][k] = fnext[q][k];
+    }
+    SegIter it(g, gridDim.x, blockIdx.x);
+    int tile, xa, xb;
+    int gs = 0;  // stage sequence number of plane xa-1 of the current segment
+    while (it.next(tile, xa, xb)) {
+      const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+      const int zb = zt0 + tz * VZ;
+      const int y = halo_warp ? (hrow == 0 ? y0 - 1 : y0 + TY) : y0 + ty;
+      const bool yok = y >= 0 && y < g.ny;
+      const int nvz = yok ? max(0, min(VZ, g.nz - zb)) : 0;
+      const long long rowbase = (long long)y * g.nz + zb;
+
+      if (halo_warp) {
+        // plane xa-1 is never read by the halo warps: hand its stage back at
+        // once (after it filled, so the arrival counts for this use), else a
+        // segment longer than the ring would starve the producer
+        wait_full(gs);
+        release(gs);
+        // halo rows of planes xa .. xb into the f-plane buffers
+        for (int x = xa; x <= xb; ++x) {
+          const int s = gs + (x - xa + 1);
+          wait_full(s);
+          CT fh[NF][VZ];
+          const bool pv = x < g.nx;
+          fields_core((int)(s % NST), hrow, pv ? nvz : 0, fh);
+          store_row(fsm + (size_t)((x - xa) & 1) * S::PLANE, hrow, fh);
+          if (x > xa) release(s - 1);
+          consumer_sync(NCONS);
         }
-      consumer_sync(NT);
+        release(gs + (xb - xa + 1));
+        gs += xb - xa + 2;
+        continue;
+      }
+
+      CT fprev[NF][VZ], fcur[NF][VZ], fnext[NF][VZ];
+      {
+        wait_full(gs);
+        fields_core((int)(gs % NST), ty + 1, (xa - 1 >= 0) ? nvz : 0, fprev);
+        wait_full(gs + 1);
+        fields_core((int)((gs + 1) % NST), ty + 1, nvz, fcur);
+        store_row(fsm, ty + 1, fcur);
+        if (own_zl || own_zr) store_zhalo(fsm, (int)((gs + 1) % NST), yok, zt0);
+      }
+      consumer_sync(NCONS);
+      release(gs);
+
+      long long gidx = (long long)xa * g.plane + rowbase;
+      for (int x = xa; x < xb; ++x, gidx += g.plane) {
+        const int s = gs + (x - xa + 1);  // stage of plane x
+        CT* bcur = fsm + (size_t)((x - xa) & 1) * S::PLANE;
+        CT* bnxt = fsm + (size_t)(((x - xa) + 1) & 1) * S::PLANE;
+        // 1. plane x+1 -> fnext + f-plane buffer (halo warps add the y-halo rows)
+        wait_full(s + 1);
+        const bool pv1 = x + 1 < g.nx;
+        fields_core((int)((s + 1) % NST), ty + 1, pv1 ? nvz : 0, fnext);
+        store_row(bnxt, ty + 1, fnext);
+        if (own_zl || own_zr) store_zhalo(bnxt, (int)((s + 1) % NST), pv1 && yok, zt0);
+        // 2. stencil(s) and epilogue of plane x
+        typename P::Epi E;
+        p.load_epi_sm(E, epi_row((int)(s % NST), ty), tz * VZ);
+        CT st[NF][VZ];
+#pragma unroll
+        for (int q = 0; q < NF; ++q) {
+          const CT* rowm = bcur + ((size_t)q * (TY + 2) + ty) * ROW + PAD + tz * VZ;
+          const CT* rowc = rowm + ROW;
+          const CT* rowp = rowc + ROW;
+          CT left[ZS], right[ZS];
+#pragma unroll
+          for (int j = 0; j < ZS; ++j) {
+            CT fromprev = __shfl_up_sync(0xffffffffu, fcur[q][VZ - ZS + j], 1);
+            CT fromnext = __shfl_down_sync(0xffffffffu, fcur[q][j], 1);
+            left[j] = (lane == 0) ? rowc[-ZS + j] : fromprev;
+            right[j] = (lane == 31) ? rowc[VZ + j] : fromnext;
+          }
+          CT ym[VZ], yp[VZ];
+#pragma unroll
+          for (int k = 0; k < VZ; ++k) {
+            ym[k] = rowm[k];
+            yp[k] = rowp[k];
+          }
+          if constexpr (HasStencilVec<P>::value) {
+            p.stencil_vec(q, fprev[q], ym, fcur[q], left, right, yp, fnext[q], st[q]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < VZ; ++k) {
+              const CT zm = (k >= ZS) ? fcur[q][k - ZS] : left[k];
+              const CT zp = (k + ZS < VZ) ? fcur[q][k + ZS] : right[k + ZS - VZ];
+              const Nb<CT> nb{fprev[q][k], ym[k], zm, fcur[q][k], zp, yp[k], fnext[q][k]};
+              st[q][k] = p.stencil(q, k, nb, fcur, E);
+            }
+          }
+        }
+        if (nvz == VZ) p.epilogue(gidx, VZ, fcur, st, E, red);
+#pragma unroll
+        for (int q = 0; q < NF; ++q)
+#pragma unroll
+          for (int k = 0; k < VZ; ++k) {
+            fprev[q][k] = fcur[q][k];
+            fcur[q][k] = fnext[q][k];
+          }
+        consumer_sync(NCONS);
+        release(s);
+      }
+      release(gs + (xb - xa + 1));  // plane xb
+      gs += xb - xa + 2;
     }
   }
 
@@ -396,7 +475,7 @@ __global__ void __launch_bounds__(P::NT + 32) sweep_tma_kernel(P p) {
     int ops[NR];
 #pragma unroll
     for (int s = 0; s < NR; ++s) ops[s] = P::op(s);
-    if (grid_finish<NR, NT + 32>(red, ops, p.partials, g.pstride, p.ticket, tot)) {
+    if (grid_finish<NR, TH::NTOT>(red, ops, p.partials, g.pstride, p.ticket, tot)) {
       if (threadIdx.x == 0) p.finalize(tot);
     }
   }
