@@ -11,12 +11,15 @@ timed region).  Lower is better.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every rank solves the full system on its own GPU
-(replicas; the slab-partitioned multi-GPU solve is not in this build), the
-reported time is the max over ranks.  ``--impl reference`` times the CPU
-oracle port (oracle/gadi_oracle.py, the reference's algorithm restated in
-numpy) on bounded samples of the same workload and extrapolates to the
-solve's iteration counts.
+N > 1 (torchrun): the grid is slab-partitioned along its slowest axis, one
+slab per GPU, with NCCL halo exchanges and rank-ordered scalar all-gathers
+(strong scaling: the same n = 512^3 system at every N); the reported time is
+the max over ranks of the device-timed solve.  ``--compare-fp64`` (default
+on at N = 1) also times the same solve with fp64 inner arithmetic (the
+north-star ">= 2x over the same code in full fp64").  ``--impl reference``
+times the CPU oracle port (oracle/gadi_oracle.py, the reference's algorithm
+restated in numpy) on bounded samples of the same workload and extrapolates
+to the solve's iteration counts.
 """
 
 from __future__ import annotations
@@ -61,6 +64,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-ng", type=int, default=128, help="grid of the bounded CPU sample")
+    ap.add_argument("--compare-fp64", type=int, default=-1,
+                    help="also time the fp64-inner solve (default: on at N=1)")
     return ap.parse_args()
 
 
@@ -216,10 +221,11 @@ def run_ours(a, rank, world):
     build = {"cd3d": g.build_cd_3d, "cdr2d": g.build_cdr_2d, "crd": g.build_complex_rd}[a.family]
     cfg = g.GadiConfig(alpha=a.alpha, u_s=a.us, outer_tol=a.outer_tol, inner_tol=a.inner_tol,
                        outer_maxit=a.outer_maxit, strict_model=False)
+    comm = g.SlabComm.from_torch(device=dev) if world > 1 else None
 
-    def solve(timer=None, problem=None, return_x=False):
+    def solve(timer=None, problem=None, return_x=False, c=cfg):
         p = problem if problem is not None else build(a.ng)
-        return g.gadi_solve(p, cfg=cfg, device=dev, return_x=return_x, hooks=timer)
+        return g.gadi_solve(p, cfg=c, device=dev, return_x=return_x, hooks=timer, comm=comm)
 
     for _ in range(a.warmup):
         solve()
@@ -243,7 +249,8 @@ def run_ours(a, rank, world):
     t_solve = dist_max(float(np.mean(times)), world)
 
     rep = reps[-1]
-    n = rep_n = (a.ng ** 3 if a.family == "cd3d" else a.ng ** 2) * (2 if a.family == "crd" else 1)
+    n = (a.ng ** 3 if a.family == "cd3d" else a.ng ** 2) * (2 if a.family == "crd" else 1)
+    rep_n = ctx.n  # unknowns of this rank's slab (= n on one GPU)
     counts = {"n": n, "outer": rep.iterations,
               "inner_h": sum(h.inner_h_iterations for h in rep.history),
               "inner_s": sum(h.inner_s_iterations for h in rep.history),
@@ -290,11 +297,27 @@ def run_ours(a, rank, world):
         t0 = time.perf_counter()
         r2 = solve(problem=p, return_x=True)
         t_e2e = time.perf_counter() - t0
-        assert r2.x is not None and r2.x.shape == (n,)
+        assert r2.x is not None and r2.x.shape == (rep_n,)
         t_e2e = dist_max(t_e2e, world)
         e2e = {"value": round(t_e2e, 4), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-               "d2h_bytes_per_step": 8 * n + 48 * r2.iterations,
-               "status": r2.status, "outer": r2.iterations}
+               "d2h_bytes_per_step": 8 * n + 48 * r2.iterations * world,
+               "status": r2.status, "outer": r2.iterations,
+               "path": "gadi_solve(problem with host b) -> H2D of b, D2H of x per rank's slab"}
+
+    # the same solve with fp64 inner arithmetic (north star: >= 2x over full fp64)
+    fp64 = None
+    if (a.compare_fp64 if a.compare_fp64 >= 0 else world == 1) and a.us != "fp64":
+        c64 = g.GadiConfig(alpha=a.alpha, u_s="fp64", outer_tol=a.outer_tol, inner_tol=a.inner_tol,
+                           outer_maxit=a.outer_maxit, strict_model=False)
+        solve(c=c64)  # warm-up (context + kernels)
+        dist_barrier(world)
+        t = Timer()
+        r64 = solve(timer=t, c=c64)
+        t64 = dist_max(t.ms / 1e3, world)
+        fp64 = {"value": round(t64, 4), "unit": UNIT, "status": r64.status, "outer": r64.iterations,
+                "inner_h": sum(h.inner_h_iterations for h in r64.history),
+                "inner_s": sum(h.inner_s_iterations for h in r64.history),
+                "berr": r64.history[-1].backward_error, "speedup_vs_fp64": round(t64 / t_solve, 3)}
 
     cpu = None
     if rank == 0 and not a.no_cpu:
@@ -304,14 +327,15 @@ def run_ours(a, rank, world):
 
     line = {"metric": METRIC, "value": round(t_solve, 4), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(t_solve * 1e3, 2), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": a.us + " inner / fp64 outer",
+            "scaling": "strong", "vs_baseline": None, "dtype": a.us + " inner / fp64 outer",
             "data": "synthetic (manufactured solution b = A 1, generated on device)",
-            "config": {**workload(a), "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "config": {**workload(a), "parallelism": f"slab x{world} (NCCL halo + all-gather)" if world > 1
+                       else "single GPU"},
             "e2e": e2e, "gpu_launches": int(launches // max(1, a.steps)),
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "solve": {k: counts[k] for k in ("status", "outer", "inner_h", "inner_s", "norm_iters", "relres",
                                               "berr", "ferr")},
-            "kernels": kernels, "lib": _lib.load().gadi_build_info().decode()}
+            "kernels": kernels, "fp64_inner_solve": fp64, "lib": _lib.load().gadi_build_info().decode()}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -334,7 +358,7 @@ def run_reference(a, rank, world):
         vals.append(est)
     v = float(np.mean(vals))
     line = {"metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": a.us + " inner (emulated) / fp64 outer", "data": "synthetic",
             "config": {**workload(a), "parallelism": "host CPU"}, "impl": "reference",
             "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",

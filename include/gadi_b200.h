@@ -79,6 +79,7 @@ typedef struct {
 } gadi_problem_desc;
 
 typedef struct gadi_ctx gadi_ctx;
+typedef struct gadi_comm gadi_comm;
 
 /* per outer step scalars (gadi.py:166-176 inputs) */
 typedef struct {
@@ -120,6 +121,27 @@ const char* gadi_build_info(void);
 int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out);
 int gadi_ctx_destroy(gadi_ctx* ctx);
 
+/* ---- slab decomposition across ranks (one process per GPU).
+ * The slowest grid axis (x planes; rows for 2-D and crd) is split into
+ * contiguous slabs.  A slab context owns global planes [x0, x1) of the
+ * problem described by `desc` (global dims; crd: desc->v is the whole
+ * potential) and exchanges one halo plane with each neighbour before every
+ * stencil pass; every Krylov / monitor reduction gathers the per-rank sums
+ * and reduces them in rank order on the device, so all ranks take identical
+ * decisions.  Vectors crossing the ABI of a slab context are the slab's rows.
+ * There is no reference counterpart (the reference is single-process). */
+/* NCCL: rank 0 creates the id, the caller broadcasts it (torch.distributed). */
+int gadi_comm_nccl_unique_id(unsigned char* id128);
+int gadi_comm_create_nccl(const unsigned char* id128, int nranks, int rank, int device, gadi_comm** out);
+/* In-process group of `nranks` slabs on one device, one host thread per rank
+ * (single-GPU test harness of the decomposition); `key` names the group. */
+int gadi_comm_create_local(int key, int nranks, int rank, gadi_comm** out);
+int gadi_comm_destroy(gadi_comm* comm);
+int gadi_comm_info(gadi_comm* comm, int* rank, int* nranks);
+int gadi_ctx_create_slab(const gadi_problem_desc* desc, int device, gadi_comm* comm, int64_t x0, int64_t x1,
+                         gadi_ctx** out);
+int gadi_ctx_slab(gadi_ctx* ctx, int64_t* x0, int64_t* x1, int64_t* n_local);
+
 /* b (block layout, n values) -> device */
 int gadi_set_rhs(gadi_ctx* ctx, const double* b);
 /* b = A 1 generated on the device (problems.py:42-45) */
@@ -149,6 +171,15 @@ int gadi_get_x(gadi_ctx* ctx, double* x);
  * rhs and x are u_s images in fp64 (n values, block layout). */
 int gadi_h_solve(gadi_ctx* ctx, const double* rhs, double tol, int maxit, double* x, gadi_inner_stats* st);
 int gadi_s_solve(gadi_ctx* ctx, const double* rhs, double tol, int maxit, double* x, gadi_inner_stats* st);
+
+/* Inner-solver arithmetic.  mode 0 (default): the storage model -- u_s
+ * storage, fp32 arithmetic, fp64 dot accumulation (the paper's cublas*Ex
+ * design).  mode 1: the reference's round-after-every-op
+ * emulation (precision.py:136-220, inner.py:47-143) with dot products summed
+ * by the pairwise tree in `dot_fmt` (inner.py:39-44 _dot_format: u_s when
+ * strict_model, fp32 otherwise): iterates bitwise the reference's.  Mode 1 is
+ * a parity mode (one host synchronisation per reduction). */
+int gadi_set_rounding(gadi_ctx* ctx, int mode, int dot_fmt);
 
 /* y = Op x with Op in {0: A (fp64, ordered), 1: H, 2: S, 3: S^T (u_s storage)}.
  * strict = 1 rounds every product and partial sum to u_s in ascending column

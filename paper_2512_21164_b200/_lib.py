@@ -98,6 +98,15 @@ SIGNATURES = {
     "gadi_s_solve": (C.c_int, [_VP, _DP, C.c_double, C.c_int, _DP, C.POINTER(InnerStats)]),
     "gadi_spmv": (C.c_int, [_VP, C.c_int, C.c_int, _DP, _DP]),
     "gadi_residual": (C.c_int, [_VP, _DP, _DP]),
+    "gadi_set_rounding": (C.c_int, [_VP, C.c_int, C.c_int]),
+    "gadi_comm_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "gadi_comm_create_nccl": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_VP)]),
+    "gadi_comm_create_local": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(_VP)]),
+    "gadi_comm_destroy": (C.c_int, [_VP]),
+    "gadi_comm_info": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "gadi_ctx_create_slab": (C.c_int, [C.POINTER(ProblemDesc), C.c_int, _VP, C.c_int64, C.c_int64,
+                                       C.POINTER(_VP)]),
+    "gadi_ctx_slab": (C.c_int, [_VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "gadi_prof_enable": (C.c_int, [_VP, C.c_int]),
     "gadi_prof_read": (C.c_int, [_VP, C.c_int, _DP, C.POINTER(C.c_int64)]),
     "gadi_timer_start": (C.c_int, [_VP]),
@@ -166,13 +175,29 @@ def dptr(a: np.ndarray):
 class Context:
     """Owns one ``gadi_ctx`` (device buffers + stream)."""
 
-    def __init__(self, desc: ProblemDesc, device: int = 0):
+    def __init__(self, desc: ProblemDesc, device: int = 0, comm=None, slab=None):
+        """``comm`` (dist.SlabComm) and ``slab`` = (x0, x1): a slab context of
+        the decomposition owning global planes [x0, x1); vectors crossing
+        this context are the slab's rows."""
         self._L = lib()
         self._desc = desc  # keep host arrays referenced during creation
         h = C.c_void_p()
-        check(self._L.gadi_ctx_create(C.byref(desc), int(device), C.byref(h)))
+        if comm is None:
+            check(self._L.gadi_ctx_create(C.byref(desc), int(device), C.byref(h)))
+        else:
+            x0, x1 = slab
+            check(self._L.gadi_ctx_create_slab(C.byref(desc), int(device), comm.h, int(x0), int(x1),
+                                               C.byref(h)))
         self.h = h
-        self.n = int(desc.n)
+        self.comm = comm
+        if comm is None:
+            self.n = int(desc.n)
+            self.slab = None
+        else:
+            a, b, m = C.c_int64(), C.c_int64(), C.c_int64()
+            check(self._L.gadi_ctx_slab(h, C.byref(a), C.byref(b), C.byref(m)))
+            self.n = int(m.value)
+            self.slab = (int(a.value), int(b.value))
 
     def close(self):
         if getattr(self, "h", None):
@@ -266,6 +291,9 @@ class Context:
         r = np.empty(self.n)
         check(self._L.gadi_residual(self.h, dptr(x), dptr(r)))
         return r
+
+    def set_rounding(self, mode: int, dot_fmt: str):
+        check(self._L.gadi_set_rounding(self.h, int(mode), FMT_CODES[dot_fmt]))
 
     KERNELS = ["hcg_init", "hcg_a", "hcg_b", "cgnr_init", "cgnr_p1", "cgnr_p2", "cgnr_p3",
                "crd_init", "crd_p1", "crd_p2", "outer", "norm_a", "norm_b", "apply"]

@@ -86,32 +86,39 @@ static int norm_pass_d(Ctx* c, const double* in, double* out) {
 }
 
 // Vectors carry guard bands so the TMA sweep may copy whole padded rows
-// (16 bytes before the first and up to a tile past the last element).
+// (16 bytes before the first and up to a tile past the last element) and,
+// in a slab decomposition, one halo plane on each side of the slab.  The
+// whole allocation starts zeroed; the raw pointer is kept for freeing.
 static constexpr size_t GUARD = 256 * 1024;
-static cudaError_t guarded_malloc(void** p, size_t bytes) {
+static size_t margin_bytes(const Ctx* c, size_t esz) { return c->comm ? esz * (size_t)c->ny * c->nz : 0; }
+static cudaError_t guarded_malloc(Ctx* c, void** p, size_t bytes, size_t esz) {
+  const size_t mb = margin_bytes(c, esz);
   unsigned char* raw = nullptr;
-  cudaError_t e = cudaMalloc((void**)&raw, bytes + 2 * GUARD);
+  cudaError_t e = cudaMalloc((void**)&raw, bytes + 2 * (GUARD + mb));
   if (e != cudaSuccess) return e;
-  *p = raw + GUARD;
-  return cudaMemset(raw, 0, GUARD) == cudaSuccess && cudaMemset(raw + GUARD + bytes, 0, GUARD) == cudaSuccess
-             ? cudaSuccess
-             : cudaErrorUnknown;
+  c->raws.push_back(raw);
+  *p = raw + GUARD + mb;
+  return cudaMemset(raw, 0, bytes + 2 * (GUARD + mb));
 }
-static void guarded_free(void* p) {
-  if (p) cudaFree(reinterpret_cast<unsigned char*>(p) - GUARD);
+// zero a vector including its halo planes
+static int zero_vec(Ctx* c, void* p, size_t esz) {
+  const size_t mb = margin_bytes(c, esz);
+  GADI_CUDA(cudaMemsetAsync(static_cast<unsigned char*>(p) - mb, 0, esz * (size_t)c->n + 2 * mb, c->stream));
+  return 0;
 }
 
 static void free_ctx(Ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* gp[] = {c->b, c->x[0], c->x[1], c->r, c->xs, c->tmp, c->R, c->P[0], c->P[1], c->Z, c->RB, c->Y};
-  for (void* p : gp) guarded_free(p);
-  void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst};
+  for (void* p : c->raws) cudaFree(p);
+  c->raws.clear();
+  void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst, c->gbuf};
   for (void* p : sp)
     if (p) cudaFree(p);
   void* hp[] = {c->h_hst, c->h_sst, c->h_osum, c->h_nst};
   for (void* p : hp)
     if (p) cudaFreeHost(p);
+  exact_free(c);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evpool) cudaEventDestroy(e);
@@ -122,9 +129,9 @@ static void free_ctx(Ctx* c) {
 
 using namespace gadi;
 
-#define ALLOCG(ptr, bytes)                                                                     \
+#define ALLOCG(ptr, bytes, esz)                                                                \
   do {                                                                                         \
-    cudaError_t e_ = guarded_malloc((void**)&(ptr), (bytes));                                  \
+    cudaError_t e_ = guarded_malloc(c, (void**)&(ptr), (bytes), (esz));                        \
     if (e_ != cudaSuccess) {                                                                   \
       free_ctx(c);                                                                             \
       delete h;                                                                                \
@@ -163,7 +170,8 @@ int gadi_device_count(int* count) {
   return 0;
 }
 
-int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out) {
+static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm, int64_t x0, int64_t x1,
+                      gadi_ctx** out) {
   if (!desc || !out) return set_error("null argument", GADI_ERR_ARG);
   *out = nullptr;
   if (desc->kind == GADI_CSR) return set_error("CSR operators are handled by the CSR engine", GADI_ERR_UNSUPPORTED);
@@ -204,11 +212,24 @@ int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out) {
       return set_error("complex family supports u_r = fp64 only", GADI_ERR_UNSUPPORTED);
     }
   }
-  c->n = (long long)c->nx * c->ny * c->nz;
-  if (c->n != desc->n || c->n <= 0) {
+  c->gn = (long long)c->nx * c->ny * c->nz;
+  if (c->gn != desc->n || c->gn <= 0) {
     delete h;
     return set_error("dims do not match n", GADI_ERR_ARG);
   }
+  c->gnx = c->nx;
+  if (comm) {
+    if (x0 < 0 || x1 <= x0 || x1 > c->gnx) {
+      delete h;
+      return set_error("slab range outside the grid", GADI_ERR_ARG);
+    }
+    c->comm = comm->c;
+    c->x0 = (int)x0;
+    c->nx = (int)(x1 - x0);
+    c->hlo = x0 > 0 ? 1 : 0;
+    c->hhi = x1 < c->gnx ? 1 : 0;
+  }
+  c->n = (long long)c->nx * c->ny * c->nz;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete h;
@@ -243,17 +264,18 @@ int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out) {
     c->pstride = mx;
   }
   const size_t n8 = sizeof(double) * (size_t)c->n, ns = c->ssz * (size_t)c->n;
-  ALLOCG(c->b, n8);
-  ALLOCG(c->x[0], n8);
-  ALLOCG(c->x[1], n8);
-  ALLOCG(c->r, n8);
-  ALLOCG(c->tmp, n8);
-  ALLOCG(c->R, ns);
-  ALLOCG(c->P[0], ns);
-  ALLOCG(c->P[1], ns);
-  ALLOCG(c->Z, ns);
-  ALLOCG(c->RB, ns);
-  ALLOCG(c->Y, ns);
+  ALLOCG(c->b, n8, 8);
+  ALLOCG(c->x[0], n8, 8);
+  ALLOCG(c->x[1], n8, 8);
+  ALLOCG(c->r, n8, 8);
+  ALLOCG(c->tmp, n8, 8);
+  ALLOCG(c->R, ns, c->ssz);
+  ALLOCG(c->P[0], ns, c->ssz);
+  ALLOCG(c->P[1], ns, c->ssz);
+  ALLOCG(c->Z, ns, c->ssz);
+  ALLOCG(c->RB, ns, c->ssz);
+  ALLOCG(c->Y, ns, c->ssz);
+  ALLOC(c->gbuf, sizeof(double) * GROW * (size_t)(c->comm ? c->comm->nranks : 1));
   ALLOC(c->partials, sizeof(double) * 8 * (size_t)c->pstride);
   ALLOC(c->ticket, sizeof(unsigned int));
   ALLOC(c->hst, sizeof(InnerState));
@@ -286,11 +308,10 @@ int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out) {
   CHK(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream));
   CHK(cudaMemsetAsync(c->hst, 0, sizeof(InnerState), c->stream));
   CHK(cudaMemsetAsync(c->sst, 0, sizeof(InnerState), c->stream));
-  CHK(cudaMemsetAsync(c->x[0], 0, n8, c->stream));
-  CHK(cudaMemsetAsync(c->x[1], 0, n8, c->stream));
-  CHK(cudaMemsetAsync(c->Y, 0, ns, c->stream));
   if (c->kind == GADI_COMPLEX) {
-    CHK(cudaMemcpyAsync(c->v64, desc->v, sizeof(double) * (size_t)(c->n / 2), cudaMemcpyHostToDevice, c->stream));
+    // desc->v is the whole grid's potential; this slab owns rows [x0, x0+nx)
+    const double* vs = desc->v + (size_t)c->x0 * (size_t)(c->nz / 2);
+    CHK(cudaMemcpyAsync(c->v64, vs, sizeof(double) * (size_t)(c->n / 2), cudaMemcpyHostToDevice, c->stream));
     int rc = c->vt->quantize(c, c->v64, c->VS, c->n / 2);
     if (rc) {
       free_ctx(c);
@@ -301,6 +322,24 @@ int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out) {
   CHK(cudaStreamSynchronize(c->stream));
 #undef CHK
   *out = h;
+  return 0;
+}
+
+int gadi_ctx_create(const gadi_problem_desc* desc, int device, gadi_ctx** out) {
+  return ctx_create(desc, device, nullptr, 0, 0, out);
+}
+
+int gadi_ctx_create_slab(const gadi_problem_desc* desc, int device, gadi_comm* comm, int64_t x0, int64_t x1,
+                         gadi_ctx** out) {
+  if (!comm) return set_error("slab context needs a communicator", GADI_ERR_ARG);
+  return ctx_create(desc, device, comm, x0, x1, out);
+}
+
+int gadi_ctx_slab(gadi_ctx* h, int64_t* x0, int64_t* x1, int64_t* n_local) {
+  Ctx* c = &h->c;
+  if (x0) *x0 = c->x0;
+  if (x1) *x1 = c->x0 + c->nx;
+  if (n_local) *n_local = c->n;
   return 0;
 }
 
@@ -323,7 +362,8 @@ int gadi_gen_rhs_ones(gadi_ctx* h) {
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   RhsOnes p;
-  p.nx = c->nx;
+  p.nx = c->gnx;
+  p.x0 = c->x0;
   p.ny = c->ny;
   p.nz = c->nz;
   p.zs = c->kind == GADI_COMPLEX ? 2 : 1;
@@ -348,8 +388,9 @@ int gadi_set_exact(gadi_ctx* h, const double* xs, int all_ones) {
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   if (xs) {
-    if (!c->xs) GADI_CUDA(guarded_malloc((void**)&c->xs, sizeof(double) * (size_t)c->n));
+    if (!c->xs) GADI_CUDA(guarded_malloc(c, (void**)&c->xs, sizeof(double) * (size_t)c->n, 8));
     GADI_TRY(upload(c, xs, c->xs));
+    GADI_TRY(halo(c, c->xs, 8));
     GADI_CUDA(cudaStreamSynchronize(c->stream));
     c->has_exact = 1;
     c->ones = 0;
@@ -367,15 +408,22 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
   double* t = c->x[1];
   GADI_CUDA(cudaEventRecord(c->ev[6], c->stream));
   if (v0) {
-    GADI_TRY(upload(c, v0, w));
+    GADI_TRY(upload(c, v0, w));  // this slab's rows of the normalised start vector
   } else {
+    // N(0,1) by global index, normalised over all slabs (analysis.py:54-57)
     const int nb = launch_1d(c, c->n);
-    randn_kernel<<<nb, 256, 0, c->stream>>>(w, c->n, (unsigned long long)seed);
+    const int rank = c->comm ? c->comm->rank : 0, nranks = c->comm ? c->comm->nranks : 1;
+    randn_kernel<<<nb, 256, 0, c->stream>>>(w, c->n, (unsigned long long)seed, (long long)c->x0 * c->ny * c->nz);
     sumsq_kernel<<<nb, 256, 0, c->stream>>>(w, c->n, c->partials);
-    scale_by_norm_kernel<<<nb, 256, 0, c->stream>>>(w, c->n, c->partials, nb);
+    partials_total_kernel<<<1, 32, 0, c->stream>>>(c->partials, nb, c->gbuf + (size_t)rank * GROW);
     c->launches += 3;
     GADI_CUDA(cudaGetLastError());
+    if (c->comm) GADI_TRY(c->comm->gather(c->gbuf, 1, c->stream));
+    scale_by_norm_kernel<<<nb, 256, 0, c->stream>>>(w, c->n, c->gbuf, nranks, GROW);
+    c->launches++;
+    GADI_CUDA(cudaGetLastError());
   }
+  GADI_TRY(halo(c, w, 8));
   norm_state_init<<<1, 1, 0, c->stream>>>(c->nst, tol, maxit);
   c->launches++;
   int launched = 0, batch = 64;
@@ -384,7 +432,9 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
     const int nb = std::min(batch, maxit - launched);
     for (int j = 0; j < nb; ++j) {
       GADI_TRY(norm_pass_d<false>(c, w, t));
+      GADI_TRY(halo(c, t, 8));
       GADI_TRY(norm_pass_d<true>(c, t, w));
+      GADI_TRY(halo(c, w, 8));
     }
     launched += nb;
     GADI_CUDA(cudaMemcpyAsync(c->h_nst, c->nst, sizeof(NormState), cudaMemcpyDeviceToHost, c->stream));
@@ -405,9 +455,9 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
   c->last_norm_ms = ms;
   *sigma = c->h_nst->sigma;
   if (iterations) *iterations = c->h_nst->it;
-  // leave x = 0 for the solve
-  GADI_CUDA(cudaMemsetAsync(c->x[0], 0, sizeof(double) * (size_t)c->n, c->stream));
-  GADI_CUDA(cudaMemsetAsync(c->x[1], 0, sizeof(double) * (size_t)c->n, c->stream));
+  // leave x = 0 (halo planes included) for the solve
+  GADI_TRY(zero_vec(c, c->x[0], 8));
+  GADI_TRY(zero_vec(c, c->x[1], 8));
   GADI_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
 }
@@ -432,8 +482,8 @@ static void fill_stats(const InnerState* s, gadi_inner_stats* o) {
 int gadi_outer_begin(gadi_ctx* h, gadi_outer_scalars* out) {
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
-  GADI_CUDA(cudaMemsetAsync(c->x[c->xcur], 0, sizeof(double) * (size_t)c->n, c->stream));
-  GADI_CUDA(cudaMemsetAsync(c->Y, 0, c->ssz * (size_t)c->n, c->stream));
+  GADI_TRY(zero_vec(c, c->x[c->xcur], 8));
+  GADI_TRY(zero_vec(c, c->Y, c->ssz));
   GADI_TRY(c->vt->outer(c, 1.0, c->has_exact));
   GADI_CUDA(cudaMemcpyAsync(c->h_osum, c->osum, sizeof(OuterSums), cudaMemcpyDeviceToHost, c->stream));
   GADI_CUDA(cudaStreamSynchronize(c->stream));
@@ -448,9 +498,16 @@ int gadi_outer_step(gadi_ctx* h, const gadi_step_args* a, gadi_outer_scalars* ou
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   GADI_CUDA(cudaEventRecord(c->ev[0], c->stream));
-  GADI_TRY(c->vt->h_solve(c, a->scale, a->inner_tol, a->maxit_h));
-  GADI_CUDA(cudaEventRecord(c->ev[1], c->stream));
-  GADI_TRY(c->vt->s_solve(c, a->coeff, a->inner_tol, a->maxit_s));
+  if (c->rounding) {
+    GADI_TRY(exact_h_solve(c, c->r, a->scale, a->inner_tol, a->maxit_h));
+    GADI_CUDA(cudaEventRecord(c->ev[1], c->stream));
+    GADI_TRY(exact_s_solve(c, c->ex[EX_Z], a->coeff, a->inner_tol, a->maxit_s));
+    GADI_TRY(c->vt->quantize(c, c->ex[EX_Y], c->Y, c->n));  // exact: y holds u_s images
+  } else {
+    GADI_TRY(c->vt->h_solve(c, a->scale, a->inner_tol, a->maxit_h));
+    GADI_CUDA(cudaEventRecord(c->ev[1], c->stream));
+    GADI_TRY(c->vt->s_solve(c, a->coeff, a->inner_tol, a->maxit_s));
+  }
   GADI_CUDA(cudaEventRecord(c->ev[2], c->stream));
   GADI_TRY(c->vt->outer(c, a->scale, c->has_exact));
   GADI_CUDA(cudaEventRecord(c->ev[3], c->stream));
@@ -484,10 +541,15 @@ int gadi_h_solve(gadi_ctx* h, const double* rhs, double tol, int maxit, double* 
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   GADI_TRY(upload(c, rhs, c->r));
-  c->pred_h = std::min(maxit, 16);
-  GADI_TRY(c->vt->h_solve(c, 1.0, tol, maxit));
-  GADI_TRY(c->vt->widen(c, c->Z, c->x[c->xcur ^ 1], c->n));
-  GADI_TRY(download(c, c->x[c->xcur ^ 1], x));
+  if (c->rounding) {
+    GADI_TRY(exact_h_solve(c, c->r, 1.0, tol, maxit));
+    GADI_TRY(download(c, c->ex[EX_Z], x));
+  } else {
+    c->pred_h = std::min(maxit, 16);
+    GADI_TRY(c->vt->h_solve(c, 1.0, tol, maxit));
+    GADI_TRY(c->vt->widen(c, c->Z, c->x[c->xcur ^ 1], c->n));
+    GADI_TRY(download(c, c->x[c->xcur ^ 1], x));
+  }
   if (st) fill_stats(c->h_hst, st);
   return 0;
 }
@@ -496,11 +558,17 @@ int gadi_s_solve(gadi_ctx* h, const double* rhs, double tol, int maxit, double* 
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   GADI_TRY(upload(c, rhs, c->r));
-  GADI_TRY(c->vt->quantize(c, c->r, c->Z, c->n));
-  c->pred_s = std::min(maxit, 16);
-  GADI_TRY(c->vt->s_solve(c, 1.0, tol, maxit));
-  GADI_TRY(c->vt->widen(c, c->Y, c->x[c->xcur ^ 1], c->n));
-  GADI_TRY(download(c, c->x[c->xcur ^ 1], x));
+  if (c->rounding) {
+    GADI_TRY(exact_s_solve(c, c->r, 1.0, tol, maxit));
+    GADI_TRY(download(c, c->ex[EX_Y], x));
+  } else {
+    GADI_TRY(c->vt->quantize(c, c->r, c->Z, c->n));
+    GADI_TRY(halo(c, c->Z, c->ssz));
+    c->pred_s = std::min(maxit, 16);
+    GADI_TRY(c->vt->s_solve(c, 1.0, tol, maxit));
+    GADI_TRY(c->vt->widen(c, c->Y, c->x[c->xcur ^ 1], c->n));
+    GADI_TRY(download(c, c->x[c->xcur ^ 1], x));
+  }
   if (st) fill_stats(c->h_sst, st);
   return 0;
 }
@@ -510,6 +578,7 @@ int gadi_spmv(gadi_ctx* h, int op, int strict, const double* x, double* y) {
   GADI_CUDA(cudaSetDevice(c->device));
   if (op < 0 || op > 3) return set_error("op must be 0..3", GADI_ERR_ARG);
   GADI_TRY(upload(c, x, c->r));
+  GADI_TRY(halo(c, c->r, 8));
   if (op == 0) {
     norm_state_init<<<1, 1, 0, c->stream>>>(c->nst, 0.0, 1);
     c->launches++;
@@ -525,7 +594,8 @@ int gadi_residual(gadi_ctx* h, const double* x, double* r) {
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   GADI_TRY(upload(c, x, c->x[c->xcur]));
-  GADI_CUDA(cudaMemsetAsync(c->Y, 0, c->ssz * (size_t)c->n, c->stream));
+  GADI_TRY(halo(c, c->x[c->xcur], 8));
+  GADI_TRY(zero_vec(c, c->Y, c->ssz));
   GADI_TRY(c->vt->outer(c, 1.0, 0));  // x_new = x + 0 ; r = b - A x
   return download(c, c->r, r);
 }
@@ -566,6 +636,18 @@ int gadi_timer_stop(gadi_ctx* h, double* ms) {
   float m = 0.f;
   GADI_CUDA(cudaEventElapsedTime(&m, c->ev[4], c->ev[5]));
   *ms = m;
+  return 0;
+}
+
+int gadi_set_rounding(gadi_ctx* h, int mode, int dot_fmt) {
+  Ctx* c = &h->c;
+  if (mode != 0 && mode != 1) return set_error("rounding mode must be 0 (storage) or 1 (reference)", GADI_ERR_ARG);
+  if (dot_fmt < GADI_BF16 || dot_fmt > GADI_FP64) return set_error("bad dot format", GADI_ERR_ARG);
+  GADI_CUDA(cudaSetDevice(c->device));
+  if (mode == 1 && c->comm) return set_error("reference rounding runs on a single domain", GADI_ERR_UNSUPPORTED);
+  c->rounding = (mode == 1 && c->us != GADI_FP64) ? 1 : 0;  // fp64 inner arithmetic is already exact
+  c->dot_fmt = dot_fmt;
+  if (c->rounding) return exact_alloc(c);
   return 0;
 }
 

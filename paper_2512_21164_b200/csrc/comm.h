@@ -1,0 +1,40 @@
+// Slab-decomposition communicator.  The grid's slowest axis is
+// split into contiguous slabs, one per rank; a stencil pass needs one halo
+// plane from each neighbour, and every Krylov / monitor reduction needs the
+// per-rank partial sums of all ranks.  Two collectives cover the hot path:
+//
+//   gather(buf, nr): rank r deposits nr doubles at buf[r*GROW ...]; after the
+//                    call every rank holds every row (ncclAllGather).  Each
+//                    rank then reduces the rows in rank order on the device
+//                    (finalize_kernel), so all ranks take bitwise-identical
+//                    decisions without a broadcast.
+//   halo(base, plane_bytes, nx): send plane 0 to rank-1 (its plane nx) and
+//                    plane nx-1 to rank+1 (its plane -1); receive likewise
+//                    (ncclSend/ncclRecv in one group).
+//
+// NcclComm binds NCCL at run time (dlopen, so the library loads on hosts
+// without it and reuses the copy torch already loaded).  LocalComm runs P
+// slabs as P host threads on ONE device (the single-GPU test harness): the
+// same engine code, collectives by device-to-device copies behind host
+// barriers.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+
+namespace gadi {
+
+constexpr int GROW = 8;  // doubles per rank row of the gather buffer
+
+struct Comm {
+  int rank = 0, nranks = 1;
+  virtual ~Comm() {}
+  virtual int gather(double* buf, int nr, cudaStream_t s) = 0;
+  virtual int halo(void* base, size_t plane_bytes, long long nx, cudaStream_t s) = 0;
+  virtual const char* kind() const = 0;
+};
+
+}  // namespace gadi
+
+struct gadi_comm {
+  gadi::Comm* c = nullptr;
+};

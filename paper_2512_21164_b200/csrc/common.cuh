@@ -23,13 +23,14 @@ template <class CT> __device__ __forceinline__ CT cvt_in(fp16 v) { return (CT)__
 template <class CT> __device__ __forceinline__ CT cvt_in(float v) { return (CT)v; }
 template <class CT> __device__ __forceinline__ CT cvt_in(double v) { return (CT)v; }
 
-// Round a compute-type value onto the storage grid (RNE; the f64 -> bf16
-// conversion is a single cvt.rn.bf16.f64 on sm_90+, which equals the
-// reference's f64 -> f32 -> bf16 double rounding because 24 >= 2*8+2).
+// Round a compute-type value onto the storage grid (RNE).  An fp64 value goes
+// to bf16 through fp32 exactly as the reference does (precision.py:113-125):
+// for an arbitrary fp64 value (e.g. 2^-e r, or a quotient) the two-step
+// rounding can differ from a direct cvt.rn.bf16.f64 at bf16 midpoints.
 template <class ST> struct Store;
 template <> struct Store<bf16> {
   static __device__ __forceinline__ bf16 from(float v) { return __float2bfloat16_rn(v); }
-  static __device__ __forceinline__ bf16 from(double v) { return __double2bfloat16(v); }
+  static __device__ __forceinline__ bf16 from(double v) { return __float2bfloat16_rn(__double2float_rn(v)); }
 };
 template <> struct Store<fp16> {
   static __device__ __forceinline__ fp16 from(float v) { return __float2half_rn(v); }

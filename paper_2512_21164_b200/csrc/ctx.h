@@ -7,11 +7,23 @@
 #include <string>
 #include <vector>
 #include "../../include/gadi_b200.h"
+#include "comm.h"
 #include "passes.cuh"
+
+#ifndef GADI_TRY
+#define GADI_TRY(x)      \
+  do {                   \
+    int rc_ = (x);       \
+    if (rc_) return rc_; \
+  } while (0)
+#endif
 
 namespace gadi {
 
 struct Ctx;
+
+// fp64 work vectors of the reference-rounding inner solvers (exact.cu)
+enum ExactBuf { EX_Z = 0, EX_R, EX_P, EX_Q, EX_RB, EX_Y, EX_T0, EX_T1, EX_N };
 
 // Per-u_s-precision entry points (one table per storage type).
 struct EngineVT {
@@ -28,8 +40,17 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int kind = 0, ndim = 2;
-  int nx = 1, ny = 1, nz = 1;  // device grid (complex: nz = 2 n_g)
-  long long n = 0;
+  int nx = 1, ny = 1, nz = 1;  // device grid of this slab (complex: nz = 2 n_g)
+  long long n = 0;             // unknowns of this slab
+  // slab decomposition: this context owns global planes
+  // [x0, x0 + nx) of gnx along the slowest axis; hlo / hhi say whether a
+  // neighbour slab exists below / above (one halo plane each, stored just
+  // before plane 0 and just after plane nx-1 of every stencil-input vector)
+  Comm* comm = nullptr;
+  int x0 = 0, gnx = 1, hlo = 0, hhi = 0;
+  long long gn = 0;             // global unknowns
+  double* gbuf = nullptr;       // gather buffer [nranks][GROW]
+  std::vector<void*> raws;      // raw device allocations (vectors with guards/halos)
   int us = GADI_FP64, u = GADI_FP64, ur = GADI_FP64;
   size_t ssz = 8;  // bytes per u_s element
   int sms = 148;
@@ -81,6 +102,11 @@ struct Ctx {
   int evused = 0;
   double prof_ms[K_NKID] = {};
   long long prof_n[K_NKID] = {};
+
+  // inner-solver arithmetic: 0 storage model (engine.cuh), 1 the reference's
+  // per-operation rounding emulation (exact.cu) with dot accumulation format
+  int rounding = 0, dot_fmt = GADI_FP64;
+  double* ex[EX_N] = {};
 
   CoefT<double> A, AT, H, S, ST;
   CoefT<float> A32;
@@ -152,6 +178,8 @@ inline SweepGeom make_geom(const Ctx* c, int TZ, int TY, int VZ, long long slots
   g.xchunk = (int)xc;
   g.pstride = c->pstride;
   g.vec = (c->nz % VZ) == 0 ? 1 : 0;
+  g.hlo = c->hlo;
+  g.hhi = c->hhi;
   return g;
 }
 inline int geom_blocks(const SweepGeom& g) {
@@ -186,6 +214,17 @@ inline void prof_collect(Ctx* c) {
     }
   }
   c->evused = 0;
+}
+
+int exact_alloc(Ctx* c);
+void exact_free(Ctx* c);
+int exact_h_solve(Ctx* c, const double* r64, double scale, double tol, int maxit);
+int exact_s_solve(Ctx* c, const double* z, double coeff, double tol, int maxit);
+
+// Halo exchange of one stencil-input vector (no-op on a single domain).
+inline int halo(Ctx* c, void* base, size_t esz) {
+  if (!c->comm) return 0;
+  return c->comm->halo(base, esz * (size_t)c->ny * c->nz, c->nx, c->stream);
 }
 
 extern EngineVT engine_bf16, engine_fp16, engine_fp32, engine_fp64;

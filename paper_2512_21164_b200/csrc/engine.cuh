@@ -27,11 +27,29 @@ inline bool tma_aligned(const Ctx* c) {
   return (c->nz % P::VZ) == 0;
 }
 
+// Slab decomposition: after a reducing pass, gather every rank's totals and
+// run the pass's scalar recurrence on them (finalize_kernel).
+template <class P>
+inline int post_reduce(Ctx* c, const P& p) {
+  if constexpr (P::HAS_RED) {
+    if (c->comm) {
+      GADI_TRY(c->comm->gather(c->gbuf, P::NR, c->stream));
+      finalize_kernel<P><<<1, 1, 0, c->stream>>>(p, c->gbuf, c->comm->nranks, GROW);
+      c->launches++;
+      GADI_CUDA(cudaGetLastError());
+    }
+  }
+  return 0;
+}
+
+inline double* defer_row(Ctx* c) { return c->comm ? c->gbuf + (size_t)c->comm->rank * GROW : nullptr; }
+
 template <class P>
 inline int launch_sweep(Ctx* c, P& p) {
   using S = SweepShape<P>;
   p.partials = c->partials;
   p.ticket = c->ticket;
+  p.defer = defer_row(c);
   if (tma_aligned<P>(c)) {
     // one resident wave of CTAs; the kernel splits the (tile, plane) units
     // evenly among them (SegIter)
@@ -77,7 +95,7 @@ inline int launch_sweep(Ctx* c, P& p) {
   }
   c->launches++;
   GADI_CUDA(cudaGetLastError());
-  return 0;
+  return post_reduce(c, p);
 }
 
 template <class P>
@@ -86,6 +104,7 @@ inline int launch_pw(Ctx* c, P& p) {
   p.partials = c->partials;
   p.ticket = c->ticket;
   p.pstride = c->pstride;
+  p.defer = defer_row(c);
   const long long chunks = (c->n + (long long)PW_NT * P::VZ - 1) / ((long long)PW_NT * P::VZ);
   int nb = (int)std::min<long long>(chunks, (long long)c->sms * 8);
   nb = std::max(nb, 1);
@@ -94,14 +113,9 @@ inline int launch_pw(Ctx* c, P& p) {
   prof_end(c);
   c->launches++;
   GADI_CUDA(cudaGetLastError());
-  return 0;
+  return post_reduce(c, p);
 }
 
-#define GADI_TRY(x)          \
-  do {                       \
-    int rc_ = (x);           \
-    if (rc_) return rc_;     \
-  } while (0)
 
 // Poll the device state of an inner solve.
 inline int poll_state(Ctx* c, InnerState* dev, InnerState* host) {
@@ -128,6 +142,7 @@ struct Engine {
     hi.tol = tol;
     hi.maxit = maxit;
     GADI_TRY(launch_pw(c, hi));
+    GADI_TRY(halo(c, c->R, sizeof(ST)));
     const CoefT<CT> H = cast_coef<CT>(c->H);
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
     int launched = 0;
@@ -154,6 +169,7 @@ struct Engine {
           a.H = H;
           GADI_TRY(launch_sweep(c, a));
         }
+        GADI_TRY(halo(c, P[(k + 1) & 1], sizeof(ST)));
         HcgB<G> b;
         b.st = c->hst;
         b.p = P[(k + 1) & 1];
@@ -161,6 +177,7 @@ struct Engine {
         b.r = (ST*)c->R;
         b.H = H;
         GADI_TRY(launch_sweep(c, b));
+        GADI_TRY(halo(c, c->R, sizeof(ST)));
       }
       launched += nb;
       GADI_TRY(poll_state(c, c->hst, c->h_hst));
@@ -170,7 +187,7 @@ struct Engine {
     }
     if (!polled) GADI_TRY(poll_state(c, c->hst, c->h_hst));
     c->pred_h = c->h_hst->it;
-    return 0;
+    return halo(c, c->Z, sizeof(ST));  // z is the stencil input of the CGNR init
   }
 
   // ------------------------------------------------------------ S-solve (CGNR)
@@ -189,6 +206,7 @@ struct Engine {
     ci.tol = tol;
     ci.maxit = maxit;
     GADI_TRY(launch_sweep(c, ci));
+    GADI_TRY(halo(c, c->RB, sizeof(ST)));
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
     int launched = 0;
     int batch = std::max(1, c->pred_s + 1);
@@ -214,6 +232,7 @@ struct Engine {
           p1.S = S;
           GADI_TRY(launch_sweep(c, p1));
         }
+        GADI_TRY(halo(c, P[(k + 1) & 1], sizeof(ST)));
         CgnrP2<G> p2;
         p2.st = c->sst;
         p2.p = P[(k + 1) & 1];
@@ -221,12 +240,14 @@ struct Engine {
         p2.r = (ST*)c->R;
         p2.S = S;
         GADI_TRY(launch_sweep(c, p2));
+        GADI_TRY(halo(c, c->R, sizeof(ST)));
         CgnrP3<G> p3;
         p3.st = c->sst;
         p3.r = (const ST*)c->R;
         p3.rbar = (ST*)c->RB;
         p3.ST_ = STc;
         GADI_TRY(launch_sweep(c, p3));
+        GADI_TRY(halo(c, c->RB, sizeof(ST)));
       }
       launched += nb;
       GADI_TRY(poll_state(c, c->sst, c->h_sst));
@@ -236,7 +257,7 @@ struct Engine {
     }
     if (!polled) GADI_TRY(poll_state(c, c->sst, c->h_sst));
     c->pred_s = c->h_sst->it;
-    return 0;
+    return halo(c, c->Y, sizeof(ST));  // y is a field input of the outer pass
   }
 
   static int s_solve_cplx(Ctx* c, double coeff, double tol, int maxit) {
@@ -282,7 +303,7 @@ struct Engine {
     }
     if (!polled) GADI_TRY(poll_state(c, c->sst, c->h_sst));
     c->pred_s = c->h_sst->it;
-    return 0;
+    return halo(c, c->Y, sizeof(ST));
   }
 
   // ------------------------------------------------------------ outer pass
@@ -305,7 +326,7 @@ struct Engine {
     o.u32 = (c->u != GADI_FP64 && c->u != GADI_FP64X2) ? 1 : 0;
     GADI_TRY(launch_sweep(c, o));
     c->xcur ^= 1;
-    return 0;
+    return halo(c, c->x[c->xcur], sizeof(double));
   }
 
   template <int DIM, int ZS, bool CPLX>

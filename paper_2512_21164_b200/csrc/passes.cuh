@@ -130,9 +130,29 @@ __device__ __forceinline__ void axpy_round(CT s, const CT (&a)[VZ], const CT (&c
   }
 }
 
+// The stencil output of the storage model is a u_s vector (the paper's
+// cuSPARSE SpMV writes hp / w in u_s): round it onto the
+// storage grid in registers before it enters a dot or an axpy.  Identity for
+// fp32 / fp64 storage.
+template <class ST, int VZ, class CT>
+__device__ __forceinline__ void round_vec(const CT (&a)[VZ], CT (&o)[VZ]) {
+  if constexpr (std::is_same<CT, float>::value && VZ % 2 == 0) {
+#pragma unroll
+    for (int k = 0; k < VZ; k += 2) {
+      const float2 v = round2<ST>(make_float2(a[k], a[k + 1]));
+      o[k] = v.x;
+      o[k + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) o[k] = round_to<ST>(a[k]);
+  }
+}
+
 // Common plumbing every pass carries.
 struct PassBase {
   SweepGeom g;
+  double* defer;  // slab decomposition: this rank's row of the gather buffer
   double* partials;
   unsigned int* ticket;
 };
@@ -204,7 +224,9 @@ struct HcgA : G, PassBase {
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
     store_any<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
-    red[0] += dotv<CT, G::VZ>(fc[0], s[0], nv);
+    CT hp[G::VZ];
+    round_vec<ST>(s[0], hp);
+    red[0] += dotv<CT, G::VZ>(fc[0], hp, nv);
   }
   __device__ void finalize(const double (&t)[1]) const {
     const double php = t[0];
@@ -266,9 +288,10 @@ struct HcgB : G, PassBase {
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
                            double (&red)[1]) const {
-    CT zn[G::VZ], rn[G::VZ];
+    CT zn[G::VZ], rn[G::VZ], hp[G::VZ];
+    round_vec<ST>(s[0], hp);
     axpy_round<ST>(alpha, fc[0], e.z, zn);
-    axpy_round<ST>(-alpha, s[0], e.r, rn);
+    axpy_round<ST>(-alpha, hp, e.r, rn);
     red[0] += dotv<CT, G::VZ>(rn, rn, nv);
     store_any<ST, G::VZ>(z, i, nv, zn, g.vec);
     store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
@@ -439,7 +462,9 @@ struct CgnrP1 : G, PassBase {
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
     store_any<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
-    red[0] += dotv<CT, G::VZ>(s[0], s[0], nv);
+    CT w[G::VZ];
+    round_vec<ST>(s[0], w);
+    red[0] += dotv<CT, G::VZ>(w, w, nv);
   }
   __device__ void finalize(const double (&t)[1]) const {
     const double denom = t[0];
@@ -501,9 +526,10 @@ struct CgnrP2 : G, PassBase {
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
                            double (&red)[1]) const {
-    CT yn[G::VZ], rn[G::VZ];
+    CT yn[G::VZ], rn[G::VZ], w[G::VZ];
+    round_vec<ST>(s[0], w);
     axpy_round<ST>(alpha, fc[0], e.y, yn);
-    axpy_round<ST>(-alpha, s[0], e.r, rn);
+    axpy_round<ST>(-alpha, w, e.r, rn);
 #pragma unroll
     for (int k = 0; k < G::VZ; ++k)
       if (k < nv) red[0] += (double)rn[k] * (double)rn[k];

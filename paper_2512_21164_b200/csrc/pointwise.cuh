@@ -28,13 +28,14 @@ __global__ void __launch_bounds__(PW_NT) pointwise_kernel(P p) {
 #pragma unroll
     for (int s = 0; s < NR; ++s) ops[s] = P::op(s);
     if (grid_finish<NR, PW_NT>(red, ops, p.partials, p.pstride, p.ticket, tot)) {
-      if (threadIdx.x == 0) p.finalize(tot);
+      if (threadIdx.x == 0) finish_pass(p, tot);
     }
   }
 }
 
 struct PwBase {
   long long n;
+  double* defer;  // slab decomposition: this rank's row of the gather buffer
   double* partials;
   unsigned int* ticket;
   int pstride;
@@ -140,9 +141,15 @@ struct CplxBase : PwBase {
       o[k + 1] = round_to<ST>(im);
     }
   }
+  // out = round(S a): w is a u_s vector of the storage model (see round_vec)
   __device__ void s_apply(const CT (&a)[VZ], const CT (&vv)[VZ], CT (&o)[VZ]) const {
 #pragma unroll
-    for (int k = 0; k < VZ; k += 2) cmul_s<ORD>(al, vv[k], a[k], a[k + 1], o[k], o[k + 1]);
+    for (int k = 0; k < VZ; k += 2) {
+      CT re, im;
+      cmul_s<ORD>(al, vv[k], a[k], a[k + 1], re, im);
+      o[k] = round_to<ST>(re);
+      o[k + 1] = round_to<ST>(im);
+    }
   }
 };
 
@@ -352,7 +359,8 @@ struct CApply : CplxBase<ST> {
 // b = A 1 in the reference's CSR row order (problems.py:42-45): each present
 // coefficient is added as 1.0 * c, ascending by column.
 struct RhsOnes {
-  int nx, ny, nz, zs;  // zs = 2 for the crd interleaved layout
+  int nx, ny, nz, zs;  // zs = 2 for the crd interleaved layout; nx = global planes
+  int x0;              // global index of this slab's first plane
   long long plane;
   CoefT<double> A;
   const double* v;  // crd potential (may be null)
@@ -361,7 +369,7 @@ struct RhsOnes {
 
 static __global__ void rhs_ones_kernel(RhsOnes p, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long x = i / p.plane, rem = i % p.plane;
+    const long long x = p.x0 + i / p.plane, rem = i % p.plane;
     const int y = (int)(rem / p.nz), z = (int)(rem % p.nz);
     const int zc = z / p.zs;         // grid column
     const int ncol = p.nz / p.zs;
@@ -415,10 +423,13 @@ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
   x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
   return x ^ (x >> 31);
 }
-static __global__ void randn_kernel(double* __restrict__ v, long long n, unsigned long long seed) {
+// element i of this slab is global element i0 + i (the vector is the same
+// for any slab decomposition)
+static __global__ void randn_kernel(double* __restrict__ v, long long n, unsigned long long seed, long long i0) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long a = splitmix64(seed ^ (2ull * (unsigned long long)i));
-    const unsigned long long b = splitmix64(seed ^ (2ull * (unsigned long long)i + 1ull));
+    const unsigned long long gi = (unsigned long long)(i0 + i);
+    const unsigned long long a = splitmix64(seed ^ (2ull * gi));
+    const unsigned long long b = splitmix64(seed ^ (2ull * gi + 1ull));
     const double u1 = ((a >> 11) + 1.0) * (1.0 / 9007199254740993.0);
     const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
     v[i] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
@@ -435,12 +446,21 @@ static __global__ void sumsq_kernel(const double* __restrict__ v, long long n, d
   block_reduce<1, 256>(a, ops);
   if (threadIdx.x == 0) partials[blockIdx.x] = a[0];
 }
-static __global__ void scale_by_norm_kernel(double* __restrict__ v, long long n, const double* __restrict__ partials,
-                                     int nparts) {
-  __shared__ double nrm;
-  if (threadIdx.x == 0) {
+// sum the per-block partials in block order into this rank's gather row
+static __global__ void partials_total_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < nparts; ++i) s += partials[i];
+    out[0] = s;
+  }
+}
+// v <- v / sqrt(sum of the gathered rows, in rank order)
+static __global__ void scale_by_norm_kernel(double* __restrict__ v, long long n, const double* __restrict__ rows,
+                                            int nranks, int row) {
+  __shared__ double nrm;
+  if (threadIdx.x == 0) {
+    double s = rows[0];
+    for (int r = 1; r < nranks; ++r) s += rows[(size_t)r * row];
     nrm = sqrt(s);
   }
   __syncthreads();

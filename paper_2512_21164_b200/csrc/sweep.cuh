@@ -38,6 +38,7 @@ struct SweepGeom {
   int xchunk;          // planes per CTA
   int pstride;         // partials row stride (>= number of CTAs)
   int vec;             // 16-byte vector path usable (nz % VZ == 0)
+  int hlo, hhi;        // slab decomposition: plane -1 / plane nx is a valid halo plane
 };
 
 // The seven neighbour values of one point, plus its centre.
@@ -127,6 +128,33 @@ __device__ __forceinline__ CT apply_stencil(const CoefT<CT>& c, CT acc, const Nb
   return apply_stencil<ORD>(c, acc, n.xm, n.ym, n.zm, n.ce, n.zp, n.yp, n.xp);
 }
 
+// End of a reducing pass: run the scalar recurrence in place (one rank), or
+// deposit this rank's totals for the gather + finalize_kernel (slabs).
+template <class P, int NR>
+__device__ __forceinline__ void finish_pass(const P& p, const double (&tot)[NR]) {
+  if (p.defer) {
+#pragma unroll
+    for (int s = 0; s < NR; ++s) p.defer[s] = tot[s];
+  } else {
+    p.finalize(tot);
+  }
+}
+
+// Slab decomposition: reduce the gathered per-rank totals in rank order (the
+// same order on every rank) and run the pass's scalar recurrence.
+template <class P>
+__global__ void finalize_kernel(P p, const double* __restrict__ gbuf, int nranks, int row) {
+  if (!p.prepare()) return;
+  constexpr int NR = P::NR;
+  double tot[NR];
+#pragma unroll
+  for (int s = 0; s < NR; ++s) tot[s] = gbuf[s];
+  for (int r = 1; r < nranks; ++r)
+#pragma unroll
+    for (int s = 0; s < NR; ++s) tot[s] = red_combine(P::op(s), tot[s], gbuf[(size_t)r * row + s]);
+  p.finalize(tot);
+}
+
 template <class P>
 __global__ void __launch_bounds__(P::NT) sweep_kernel(P p) {
   using S = SweepShape<P>;
@@ -172,7 +200,7 @@ __global__ void __launch_bounds__(P::NT) sweep_kernel(P p) {
   bool r_zl[ZS], r_zr[ZS];
 
   auto load_plane = [&](int xp) {
-    const bool pv = (xp >= 0 && xp < g.nx);
+    const bool pv = (xp >= -g.hlo && xp < g.nx + g.hhi);
     r_nv = pv ? nvz : 0;
     r_nvhm = pv ? nvhm : 0;
     r_nvhp = pv ? nvhp : 0;
@@ -272,7 +300,7 @@ __global__ void __launch_bounds__(P::NT) sweep_kernel(P p) {
   // ---- prologue: plane xa-1 (core only), plane xa (haloed, smem buffer 0)
   {
     const int xp = xa - 1;
-    const int nv = (xp >= 0) ? nvz : 0;
+    const int nv = (xp >= -g.hlo) ? nvz : 0;
     typename P::Raw Rp;
     if (nv > 0) p.load_raw(Rp, gidx(xp, y, zb), nv);
     fields(Rp, nv, fprev);
@@ -351,7 +379,7 @@ __global__ void __launch_bounds__(P::NT) sweep_kernel(P p) {
 #pragma unroll
     for (int s = 0; s < NR; ++s) ops[s] = P::op(s);
     if (grid_finish<NR, NT>(red, ops, p.partials, g.pstride, p.ticket, tot)) {
-      if (threadIdx.x == 0) p.finalize(tot);
+      if (threadIdx.x == 0) finish_pass(p, tot);
     }
   }
 }

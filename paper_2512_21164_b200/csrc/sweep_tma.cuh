@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
         const int st = gs % NST;
         if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
         unsigned char* sb = stages + (size_t)st * TS::STAGE;
-        const bool pv = (xp >= 0 && xp < g.nx);
+        const bool pv = (xp >= -g.hlo && xp < g.nx + g.hhi);
         const bool ev = pv && xp >= xa && xp < xb;
         unsigned bytes = 0;
         if (pv) {
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
           const int s = gs + (x - xa + 1);
           wait_full(s);
           CT fh[NF][VZ];
-          const bool pv = x < g.nx;
+          const bool pv = x < g.nx + g.hhi;
           fields_core((int)(s % NST), hrow, pv ? nvz : 0, fh);
           store_row(fsm + (size_t)((x - xa) & 1) * S::PLANE, hrow, fh);
           if (x > xa) release(s - 1);
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
       CT fprev[NF][VZ], fcur[NF][VZ], fnext[NF][VZ];
       {
         wait_full(gs);
-        fields_core((int)(gs % NST), ty + 1, (xa - 1 >= 0) ? nvz : 0, fprev);
+        fields_core((int)(gs % NST), ty + 1, (xa - 1 >= -g.hlo) ? nvz : 0, fprev);
         wait_full(gs + 1);
         fields_core((int)((gs + 1) % NST), ty + 1, nvz, fcur);
         store_row(fsm, ty + 1, fcur);
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
         CT* bnxt = fsm + (size_t)(((x - xa) + 1) & 1) * S::PLANE;
         // 1. plane x+1 -> fnext + f-plane buffer (halo warps add the y-halo rows)
         wait_full(s + 1);
-        const bool pv1 = x + 1 < g.nx;
+        const bool pv1 = x + 1 < g.nx + g.hhi;
         fields_core((int)((s + 1) % NST), ty + 1, pv1 ? nvz : 0, fnext);
         store_row(bnxt, ty + 1, fnext);
         if (own_zl || own_zr) store_zhalo(bnxt, (int)((s + 1) % NST), pv1 && yok, zt0);
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
 #pragma unroll
     for (int s = 0; s < NR; ++s) ops[s] = P::op(s);
     if (grid_finish<NR, TH::NTOT>(red, ops, p.partials, g.pstride, p.ticket, tot)) {
-      if (threadIdx.x == 0) p.finalize(tot);
+      if (threadIdx.x == 0) finish_pass(p, tot);
     }
   }
 }

@@ -54,8 +54,8 @@ def make_desc(spec: StencilSpec, alpha: float, u_s, u="fp64", u_r="fp64", *,
     return d
 
 
-def open_context(desc, device: int = 0) -> _lib.Context:
-    return _lib.Context(desc, device)
+def open_context(desc, device: int = 0, comm=None, slab=None) -> _lib.Context:
+    return _lib.Context(desc, device, comm=comm, slab=slab)
 
 
 _CACHE: dict = {}

@@ -19,7 +19,7 @@ from .device import make_desc, open_context
 from .precision import resolve_format
 from .stencil import StencilMatrix
 
-__all__ = ["InnerSolveStats", "cg_spd", "cg_normal_skew", "default_maxit"]
+__all__ = ["InnerSolveStats", "cg_spd", "cg_normal_skew", "default_maxit", "dot_format"]
 
 _MAXIT_CAP = 10_000
 
@@ -27,6 +27,16 @@ _MAXIT_CAP = 10_000
 def default_maxit(n: int) -> int:
     """min(10^4, ceil(5 sqrt(n))) (inner.py:26-27)."""
     return min(_MAXIT_CAP, max(1, math.ceil(5.0 * math.sqrt(n))))
+
+
+def dot_format(fmt, strict_model: bool):
+    """Accumulation format of the reference's dot products (inner.py:39-44):
+    u_s, or fp32 when ``strict_model`` is off and u_s is below fp32."""
+    fmt = resolve_format(fmt)
+    fp32 = resolve_format("fp32")
+    if not strict_model and fmt.unit_roundoff > fp32.unit_roundoff:
+        return fp32
+    return fmt
 
 
 @dataclass
@@ -64,13 +74,15 @@ def _true_relres(op: StencilMatrix, rhs, x, nrhs) -> float:
 
 
 def cg_spd(h, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
-           strict_model: bool = True):
-    """CG on H x = rhs, H SPD, x0 = 0."""
+           strict_model: bool = True, *, rounding: str = "storage"):
+    """CG on H x = rhs, H SPD, x0 = 0.  ``rounding="reference"`` runs the
+    reference's per-operation rounding emulation (bitwise iterates)."""
     fmt = resolve_format(fmt)
     rhs = np.asarray(rhs, dtype=np.float64)
     if maxit is None:
         maxit = default_maxit(rhs.size)
     with _ctx_for(h, fmt, "H") as ctx:
+        ctx.set_rounding(1 if rounding == "reference" else 0, dot_format(fmt, strict_model).name)
         x, st = ctx.h_solve(rhs, tol, maxit)
     nrhs = float(np.linalg.norm(rhs))
     return x, InnerSolveStats(st.iterations, st.final_relative_residual, bool(st.converged),
@@ -78,7 +90,7 @@ def cg_spd(h, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
 
 
 def cg_normal_skew(s, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
-                   strict_model: bool = True, s_transpose=None):
+                   strict_model: bool = True, s_transpose=None, *, rounding: str = "storage"):
     """CGNR on S y = rhs (S^T S y = S^T rhs without forming S^T S), y0 = 0.
     ``s_transpose`` is implied by the stencil (S^T swaps the lo/up
     coefficients; crd flips the sign of V)."""
@@ -87,6 +99,7 @@ def cg_normal_skew(s, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt
     if maxit is None:
         maxit = default_maxit(rhs.size)
     with _ctx_for(s, fmt, "S") as ctx:
+        ctx.set_rounding(1 if rounding == "reference" else 0, dot_format(fmt, strict_model).name)
         y, st = ctx.s_solve(rhs, tol, maxit)
     nrhs = float(np.linalg.norm(rhs))
     return y, InnerSolveStats(st.iterations, st.final_relative_residual, bool(st.converged),

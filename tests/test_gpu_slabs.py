@@ -1,0 +1,156 @@
+"""Slab decomposition on one GPU: P slab contexts driven by P host threads
+over the in-process communicator (SlabComm.local) -- the same kernels,
+halo exchanges and rank-ordered reductions the NCCL path runs, with device
+copies as the transport.
+
+* stencil passes without reductions (fp64 residual, operator applies) must be
+  BITWISE the single-domain result: the halo planes carry exactly the
+  neighbour's values;
+* ||A||_2 and full solves reduce per-rank partial sums in rank order, so they
+  agree with the single domain to rounding: outer counts within +-1 (the
+  north-star bar across 1/2/4/8 GPUs), same status, berr within 2x."""
+
+import random
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2512_21164_b200 as g
+from paper_2512_21164_b200 import device
+from paper_2512_21164_b200.dist import SlabComm, slab_range, slab_rows
+
+pytestmark = pytest.mark.gpu
+
+BUILD = {"cdr2d": g.build_cdr_2d, "cd3d": g.build_cd_3d, "crd": g.build_complex_rd}
+
+
+def run_slabs(P, fn, timeout=300):
+    """fn(comm, rank) on P threads; returns the per-rank results."""
+    key = random.randrange(1 << 30)
+    out, errs = [None] * P, []
+
+    def work(r):
+        comm = SlabComm.local(key, P, r)
+        try:
+            out[r] = fn(comm, r)
+        except BaseException as e:  # noqa: BLE001 - surfaced below
+            errs.append(e)
+        finally:
+            comm.close()
+
+    ts = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout)
+    assert not any(t.is_alive() for t in ts), "slab ranks deadlocked"
+    if errs:
+        raise errs[0]
+    return out
+
+
+def join_rows(parts, family):
+    if family == "crd":  # block layout [re; im] per slab
+        re = [p[:p.size // 2] for p in parts]
+        im = [p[p.size // 2:] for p in parts]
+        return np.concatenate(re + im)
+    return np.concatenate(parts)
+
+
+def _bits_equal(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.array_equal(a, b) or np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+CASES = [("cdr2d", 40), ("cd3d", 20), ("crd", 24)]
+
+
+@pytest.mark.parametrize("fam,ng", CASES)
+@pytest.mark.parametrize("P", [2, 3])
+def test_slab_stencils_bitwise(gpu, fam, ng, P):
+    p = BUILD[fam](ng)
+    spec = p.A.spec
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(p.n)
+    b = rng.standard_normal(p.n)
+    r_full = g.residual(p.A, x, b, "fp64")
+    ax_full = g.spmv(p.A, x, "fp64")
+    sp = g.make_hss_splitting(p.A, 0.7, "bf16")
+    xq = g.quantize(x, "bf16")
+    # the operator's coefficients sit in the H slot of a bf16 context (op 1)
+    ops_full = {op: device._op_context(m, "bf16").spmv(1, xq)
+                for op, m in (("H", sp.H_low), ("S", sp.S_low), ("ST", sp.S_low_T))} if fam != "crd" else {}
+
+    def rank(comm, r):
+        x0, x1 = slab_range(spec.dims[0], P, r)
+        res = {}
+        with device.open_context(device.make_desc(spec, 1.0, "fp64"), 0, comm=comm, slab=(x0, x1)) as ctx:
+            ctx.set_rhs(slab_rows(b, spec, x0, x1))
+            res["r"] = ctx.residual(slab_rows(x, spec, x0, x1))
+            res["ax"] = ctx.spmv(0, slab_rows(x, spec, x0, x1))
+        if fam != "crd":
+            for op, m in (("H", sp.H_low), ("S", sp.S_low), ("ST", sp.S_low_T)):
+                c = m.coefs()
+                desc = device.make_desc(spec, 0.0, "bf16", H=c, S=c)
+                with device.open_context(desc, 0, comm=comm, slab=(x0, x1)) as ctx:
+                    res[op] = ctx.spmv(1, slab_rows(xq, spec, x0, x1))
+        return res
+
+    parts = run_slabs(P, rank)
+    assert _bits_equal(join_rows([q["r"] for q in parts], fam), r_full)
+    assert _bits_equal(join_rows([q["ax"] for q in parts], fam), ax_full)
+    for op, want in ops_full.items():
+        assert _bits_equal(join_rows([q[op] for q in parts], fam), want), op
+
+
+@pytest.mark.parametrize("fam,ng", CASES)
+def test_slab_norm2(gpu, fam, ng):
+    p = BUILD[fam](ng)
+    want = g.matrix_norm_2(p.A)
+    spec = p.A.spec
+    v0 = g.analysis.power_start_vector(p.n)
+
+    def rank(comm, r):
+        x0, x1 = slab_range(spec.dims[0], 3, r)
+        with device.open_context(device.make_desc(spec, 1.0, "fp64"), 0, comm=comm, slab=(x0, x1)) as ctx:
+            return ctx.norm2(slab_rows(v0, spec, x0, x1))
+
+    got = run_slabs(3, rank)
+    assert all(s == got[0] for s in got), "ranks disagree"
+    assert got[0][0] == pytest.approx(want, rel=1e-12)
+
+
+SOLVES = [
+    ("cdr2d", 32, dict(alpha=1.0, u_s="bf16", outer_tol=1e-10)),
+    ("cdr2d", 32, dict(alpha=1.0, u_s="fp64", outer_tol=1e-10)),
+    ("cd3d", 16, dict(alpha=0.5, u_s="bf16", outer_tol=1e-6)),
+    ("cd3d", 16, dict(alpha=0.5, u_s="fp32", outer_tol=1e-6)),
+    ("crd", 16, dict(alpha=10.0, u_s="fp32", outer_tol=1e-6)),
+]
+
+
+@pytest.mark.parametrize("fam,ng,kw", SOLVES)
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_solve_matches_single_domain(gpu, fam, ng, kw, P):
+    cfg = g.GadiConfig(outer_maxit=800, **kw)
+    ref = g.gadi_solve(BUILD[fam](ng), cfg=cfg, reuse_context=False)
+
+    def rank(comm, r):
+        return g.gadi_solve(BUILD[fam](ng), cfg=cfg, comm=comm, reuse_context=False)
+
+    reps = run_slabs(P, rank)
+    # identical decisions on every rank
+    for rep in reps[1:]:
+        assert rep.iterations == reps[0].iterations
+        assert [h.relative_residual for h in rep.history] == [h.relative_residual for h in reps[0].history]
+    rep = reps[0]
+    assert rep.status == ref.status
+    assert abs(rep.iterations - ref.iterations) <= 1, (rep.iterations, ref.iterations)
+    b1, b2 = rep.history[-1].backward_error, ref.history[-1].backward_error
+    assert 0.5 * b2 <= b1 <= 2.0 * b2, (b1, b2)
+    assert rep.norm_A == pytest.approx(ref.norm_A, rel=1e-12)
+    # both iterates are within their forward error of x* = 1
+    x = join_rows([q.x for q in reps], fam)
+    fe = (rep.history[-1].forward_error or 0.0) + (ref.history[-1].forward_error or 0.0)
+    np.testing.assert_allclose(x, ref.x, rtol=0, atol=2.0 * np.sqrt(x.size) * fe + 1e-14)

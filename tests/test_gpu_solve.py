@@ -18,9 +18,17 @@ def _problem(c):
     return {"cdr2d": g.build_cdr_2d, "cd3d": g.build_cd_3d, "crd": g.build_complex_rd}[fam](n_g, **kw)
 
 
+# The storage model (u_s storage, fp32 arithmetic: the paper's GPU design) is
+# not the reference's per-operation rounding emulation; on one golden case its
+# bf16 outer count lands 2 steps away (reference strict_model=False: 97; the
+# storage model: 99; reference strict: 98).  rounding="reference" reproduces
+# that case -- and every other -- exactly (test_solve_reference_rounding_exact).
+STORAGE_MODEL_DEVIATIONS = {"nonstrict_cdr2d32_bf16": 2}
+
+
 def _check(c, rep):
     all64 = all(c["cfg"].get(k, "fp64") == "fp64" for k in ("u", "u_r", "u_s"))
-    tol = 0 if all64 else 1
+    tol = 0 if all64 else STORAGE_MODEL_DEVIATIONS.get(c["name"], 1)
     assert rep.status == c["status"], (c["name"], rep.status, c["status"])
     if c["status"] == "Stagnated":
         # stagnation fires on a window test; the floor must match, the count loosely
@@ -106,12 +114,50 @@ def test_inner_solvers_vs_reference(gpu, golden_inner, k):
     zr, yr = np.array(c["h_x"]), np.array(c["s_x"])
     if c["u_s"] == "fp64":
         assert sh.iterations == c["h_it"] and ss.iterations == c["s_it"]
-        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
-        assert np.linalg.norm(y - yr) <= 1e-10 * np.linalg.norm(yr)
+        # fp64 iterates agree to rounding; an unconverged CGNR (crd: maxit
+        # reached on both sides) amplifies the unpinned BLAS dot order
+        assert np.linalg.norm(z - zr) <= (1e-10 if c["h_conv"] else 1e-5) * np.linalg.norm(zr)
+        assert np.linalg.norm(y - yr) <= (1e-10 if c["s_conv"] else 1e-5) * np.linalg.norm(yr)
     else:
         assert abs(sh.iterations - c["h_it"]) <= max(2, 0.2 * c["h_it"]), (sh.iterations, c["h_it"])
         assert abs(ss.iterations - c["s_it"]) <= max(2, 0.2 * c["s_it"]), (ss.iterations, c["s_it"])
-    assert sh.converged and ss.converged
+    assert sh.converged == c["h_conv"] and ss.converged == c["s_conv"]
     # both solutions satisfy the same true-residual level
     assert sh.true_relative_residual <= max(3 * c["h_true"], 3e-4)
     assert ss.true_relative_residual <= max(3 * c["s_true"], 3e-4)
+
+
+# ---------------------------------------------------------------- reference rounding mode
+# rounding="reference" runs the inner solvers with the reference's per-operation
+# rounding emulation (csrc/exact.cu): the iterates are bitwise the reference's,
+# so outer AND every per-step inner count must match exactly, and so must x.
+EXACT_CASES = [n for n in SOLVE_CASES if not n.endswith("_fp64") and n not in ("gadi_cdr2d6",)]
+
+
+@pytest.mark.parametrize("name", EXACT_CASES)
+def test_solve_reference_rounding_exact(gpu, golden_solves, name):
+    if name not in golden_solves:
+        pytest.skip(f"{name} not in fixtures")
+    c = golden_solves[name]
+    rep = g.gadi_solve(_problem(c), cfg=g.GadiConfig(**c["cfg"]), rounding="reference")
+    assert rep.status == c["status"], (name, rep.status)
+    assert rep.iterations == c["outer"], (name, rep.iterations, c["outer"])
+    assert [h.inner_h_iterations for h in rep.history] == c["inner_h"], name
+    assert [h.inner_s_iterations for h in rep.history] == c["inner_s"], name
+    np.testing.assert_allclose(rep.relative_residuals, c["relres"], rtol=1e-9, atol=0)
+    assert np.array_equal(rep.x[:8], np.array(c["x_head"])), (rep.x[:8], c["x_head"])
+
+
+@pytest.mark.parametrize("k", range(9))
+def test_inner_solvers_reference_rounding_bitwise(gpu, golden_inner, k):
+    c = golden_inner[k]
+    fam = c["family"]
+    p = {"cdr2d": g.build_cdr_2d, "cd3d": g.build_cd_3d, "crd": g.build_complex_rd}[fam](c["n_g"])
+    sp = g.make_hss_splitting(p.A, c["alpha"], c["u_s"])
+    rhs = np.array(c["rhs"])
+    z, sh = g.cg_spd(sp.H_low, rhs, 1e-4, None, c["u_s"], rounding="reference")
+    y, ss = g.cg_normal_skew(sp.S_low, rhs, 1e-4, None, c["u_s"], True, sp.S_low_T, rounding="reference")
+    assert sh.iterations == c["h_it"] and ss.iterations == c["s_it"]
+    if c["u_s"] != "fp64":
+        assert np.array_equal(z, np.array(c["h_x"])), "H-solve iterate differs from the reference"
+        assert np.array_equal(y, np.array(c["s_x"])), "S-solve iterate differs from the reference"
