@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .device import make_desc, open_context
+from .device import is_csr, make_csr_desc, make_desc, open_context
 from .errors import ZeroError, ZeroReference
 from .stencil import StencilMatrix
 
@@ -37,6 +37,10 @@ def power_start_vector(n: int):
 
 
 def matrix_norm_2(a, tol: float = _POWER_TOL, maxit: int = _POWER_MAXIT) -> float:
+    if is_csr(a):
+        with open_context(make_csr_desc(a, a, a, a, "fp64")) as ctx:
+            sigma, _ = ctx.norm2(power_start_vector(a.nrows), _POWER_SEED, tol, maxit)
+        return sigma
     if not isinstance(a, StencilMatrix) or a.role != "A":
         raise NotImplementedError("matrix_norm_2 runs on stencil system matrices")
     with open_context(make_desc(a.spec, 1.0, "fp64")) as ctx:

@@ -80,6 +80,15 @@ static int norm_pass(Ctx* c, const double* in, double* out) {
 
 template <bool TRANS>
 static int norm_pass_d(Ctx* c, const double* in, double* out) {
+  if (c->kind == GADI_CSR) {
+    const CsrDev& m = c->csr[TRANS ? CS_AT : CS_A];
+    CsrNorm<TRANS> p;
+    p.ns = c->nst;
+    p.M = CsrT<double>{m.rp, m.ci, m.v64};
+    p.in = in;
+    p.outv = out;
+    return launch_pw(c, p);
+  }
   if (c->kind == GADI_COMPLEX) return norm_pass<2, 2, true, TRANS>(c, in, out);
   if (c->ndim == 3) return norm_pass<3, 1, false, TRANS>(c, in, out);
   return norm_pass<2, 1, false, TRANS>(c, in, out);
@@ -112,6 +121,12 @@ static void free_ctx(Ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->raws) cudaFree(p);
   c->raws.clear();
+  for (CsrDev& m : c->csr) {
+    void* cp[] = {m.rp, m.ci, m.v64, m.vs};
+    for (void* p : cp)
+      if (p) cudaFree(p);
+    m = CsrDev();
+  }
   void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst, c->gbuf};
   for (void* p : sp)
     if (p) cudaFree(p);
@@ -170,12 +185,58 @@ int gadi_device_count(int* count) {
   return 0;
 }
 
+// Upload one CSR operator (int64 offsets, int32 columns, fp64 values; the
+// u_s copy is made by the engine's quantize kernel).  `transpose` uploads
+// the transpose instead (ascending columns by construction).
+static int upload_csr(Ctx* c, const gadi_csr& h, CsrDev& d, bool transpose, bool typed) {
+  if (!h.row_offsets || !h.col_indices || !h.values || h.nrows != c->n)
+    return set_error("CSR operator missing or of the wrong size", GADI_ERR_ARG);
+  const long long n = h.nrows, nnz = h.nnz;
+  if (n >= (1LL << 31)) return set_error("CSR operators need fewer than 2^31 rows", GADI_ERR_UNSUPPORTED);
+  std::vector<long long> rp(n + 1);
+  std::vector<int> ci((size_t)nnz);
+  std::vector<double> v((size_t)nnz);
+  if (!transpose) {
+    for (long long i = 0; i <= n; ++i) rp[i] = h.row_offsets[i];
+    for (long long k = 0; k < nnz; ++k) {
+      ci[k] = (int)h.col_indices[k];
+      v[k] = h.values[k];
+    }
+  } else {
+    std::fill(rp.begin(), rp.end(), 0LL);
+    for (long long k = 0; k < nnz; ++k) rp[h.col_indices[k] + 1]++;
+    for (long long i = 0; i < n; ++i) rp[i + 1] += rp[i];
+    std::vector<long long> pos(rp.begin(), rp.end() - 1);
+    for (long long i = 0; i < n; ++i)
+      for (long long k = h.row_offsets[i]; k < h.row_offsets[i + 1]; ++k) {
+        const long long dst = pos[h.col_indices[k]]++;
+        ci[dst] = (int)i;
+        v[dst] = h.values[k];
+      }
+  }
+  d.nnz = nnz;
+  GADI_CUDA(cudaMalloc((void**)&d.rp, sizeof(long long) * (size_t)(n + 1)));
+  GADI_CUDA(cudaMalloc((void**)&d.ci, sizeof(int) * (size_t)std::max(1LL, nnz)));
+  GADI_CUDA(cudaMalloc((void**)&d.v64, sizeof(double) * (size_t)std::max(1LL, nnz)));
+  GADI_CUDA(cudaMemcpy(d.rp, rp.data(), sizeof(long long) * (size_t)(n + 1), cudaMemcpyHostToDevice));
+  if (nnz) {
+    GADI_CUDA(cudaMemcpy(d.ci, ci.data(), sizeof(int) * (size_t)nnz, cudaMemcpyHostToDevice));
+    GADI_CUDA(cudaMemcpy(d.v64, v.data(), sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice));
+  }
+  if (typed) {
+    GADI_CUDA(cudaMalloc(&d.vs, c->ssz * (size_t)std::max(1LL, nnz)));
+    if (nnz) GADI_TRY(c->vt->quantize(c, d.v64, d.vs, nnz));
+  }
+  return 0;
+}
+
 static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm, int64_t x0, int64_t x1,
                       gadi_ctx** out) {
   if (!desc || !out) return set_error("null argument", GADI_ERR_ARG);
   *out = nullptr;
-  if (desc->kind == GADI_CSR) return set_error("CSR operators are handled by the CSR engine", GADI_ERR_UNSUPPORTED);
-  if (desc->kind != GADI_STENCIL && desc->kind != GADI_COMPLEX) return set_error("unknown kind", GADI_ERR_ARG);
+  if (desc->kind != GADI_STENCIL && desc->kind != GADI_COMPLEX && desc->kind != GADI_CSR)
+    return set_error("unknown kind", GADI_ERR_ARG);
+  if (desc->kind == GADI_CSR && comm) return set_error("CSR operators run on a single domain", GADI_ERR_UNSUPPORTED);
   EngineVT* vt = engine_for(desc->u_s);
   if (!vt) return set_error("u_s must be bf16, fp16, fp32 or fp64", GADI_ERR_ARG);
   gadi_ctx* h = new gadi_ctx();
@@ -194,7 +255,13 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   if (getenv("GADI_WAVES")) c->waves = std::max(1, atoi(getenv("GADI_WAVES")));
   if (getenv("GADI_MIN_CHUNK")) c->min_chunk = std::max(1, atoi(getenv("GADI_MIN_CHUNK")));
   if (getenv("GADI_LOCKSTEP")) c->lockstep = atoi(getenv("GADI_LOCKSTEP"));
-  if (c->kind == GADI_STENCIL) {
+  if (c->kind == GADI_CSR) {
+    // rows as a 1-D "grid" (no stencil geometry is used)
+    c->nx = (int)desc->csr_A.nrows;
+    c->ny = 1;
+    c->nz = 1;
+    c->ndim = 1;
+  } else if (c->kind == GADI_STENCIL) {
     c->nx = (int)desc->dims[0];
     c->ny = (int)desc->dims[1];
     c->nz = (int)desc->dims[2];
@@ -319,6 +386,17 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
       return rc;
     }
   }
+  if (c->kind == GADI_CSR) {
+    const gadi_csr* ops[CS_N] = {&desc->csr_A, &desc->csr_A, &desc->csr_H, &desc->csr_S, &desc->csr_ST};
+    for (int s = 0; s < CS_N; ++s) {
+      int rc = upload_csr(c, *ops[s], c->csr[s], s == CS_AT, s >= CS_H);
+      if (rc) {
+        free_ctx(c);
+        delete h;
+        return rc;
+      }
+    }
+  }
   CHK(cudaStreamSynchronize(c->stream));
 #undef CHK
   *out = h;
@@ -360,6 +438,7 @@ int gadi_set_rhs(gadi_ctx* h, const double* b) {
 
 int gadi_gen_rhs_ones(gadi_ctx* h) {
   Ctx* c = &h->c;
+  if (c->kind == GADI_CSR) return set_error("b = A 1 is generated for stencil families only", GADI_ERR_UNSUPPORTED);
   GADI_CUDA(cudaSetDevice(c->device));
   RhsOnes p;
   p.nx = c->gnx;

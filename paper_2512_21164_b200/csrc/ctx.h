@@ -22,6 +22,16 @@ namespace gadi {
 
 struct Ctx;
 
+// general-CSR operators (kind GADI_CSR): A, A^T (power iteration), H, S, S^T
+enum CsrSlot { CS_A = 0, CS_AT, CS_H, CS_S, CS_ST, CS_N };
+struct CsrDev {
+  long long* rp = nullptr;  // nrows + 1
+  int* ci = nullptr;        // nnz
+  double* v64 = nullptr;    // fp64 values (u_s images for H, S, S^T)
+  void* vs = nullptr;       // values in u_s storage (H, S, S^T)
+  long long nnz = 0;
+};
+
 // fp64 work vectors of the reference-rounding inner solvers (exact.cu)
 enum ExactBuf { EX_Z = 0, EX_R, EX_P, EX_Q, EX_RB, EX_Y, EX_T0, EX_T1, EX_N };
 
@@ -107,6 +117,7 @@ struct Ctx {
   // per-operation rounding emulation (exact.cu) with dot accumulation format
   int rounding = 0, dot_fmt = GADI_FP64;
   double* ex[EX_N] = {};
+  CsrDev csr[CS_N];
 
   CoefT<double> A, AT, H, S, ST;
   CoefT<float> A32;

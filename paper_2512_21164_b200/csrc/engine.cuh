@@ -11,8 +11,8 @@
 // `done` flag once per batch.
 #pragma once
 #include <algorithm>
+#include "csr.cuh"
 #include "ctx.h"
-#include "pointwise.cuh"
 
 namespace gadi {
 
@@ -125,9 +125,161 @@ inline int poll_state(Ctx* c, InnerState* dev, InnerState* host) {
   return 0;
 }
 
+// Enqueue inner iterations in batches (the previous solve's count + 1 first,
+// then a quarter of it), polling the device `done` flag once per batch.
+// iter(k) enqueues iteration k; passes launched after convergence are no-ops.
+template <class F>
+inline int run_batched(Ctx* c, InnerState* dev, InnerState* host, int& pred, int maxit, F&& iter) {
+  int launched = 0, batch = std::max(1, pred + 1);
+  bool polled = false;
+  while (launched < maxit) {
+    const int nb = std::min(batch, maxit - launched);
+    for (int j = 0; j < nb; ++j) GADI_TRY(iter(launched + j));
+    launched += nb;
+    GADI_TRY(poll_state(c, dev, host));
+    polled = true;
+    if (host->done) break;
+    batch = std::max(2, pred / 4 + 1);
+  }
+  if (!polled) GADI_TRY(poll_state(c, dev, host));
+  pred = host->it;
+  return 0;
+}
+
 template <class ST>
 struct Engine {
   typedef typename CTOf<ST>::type CT;
+
+  // ------------------------------------------------------------ general CSR (csr.cuh)
+  static CsrT<ST> csr_s(const Ctx* c, int slot) {
+    return CsrT<ST>{c->csr[slot].rp, c->csr[slot].ci, (const ST*)c->csr[slot].vs};
+  }
+  static CsrT<double> csr_d(const Ctx* c, int slot) {
+    return CsrT<double>{c->csr[slot].rp, c->csr[slot].ci, c->csr[slot].v64};
+  }
+  static int h_solve_csr(Ctx* c, double scale, double tol, int maxit) {
+    HcgInit<ST> hi;
+    hi.r64 = c->r;
+    hi.rs = (ST*)c->R;
+    hi.z = (ST*)c->Z;
+    hi.st = c->hst;
+    hi.scale = scale;
+    hi.tol = tol;
+    hi.maxit = maxit;
+    GADI_TRY(launch_pw(c, hi));
+    const CsrT<ST> H = csr_s(c, CS_H);
+    ST* p = (ST*)c->P[0];
+    ST* q = (ST*)c->P[1];
+    return run_batched(c, c->hst, c->h_hst, c->pred_h, maxit, [&](int k) {
+      CsrDir<ST> d;
+      d.st = c->hst;
+      d.f = (const ST*)c->R;
+      d.p = p;
+      d.first = k == 0;
+      GADI_TRY(launch_pw(c, d));
+      CsrSpmv<ST, 0> s;
+      s.st = c->hst;
+      s.m = H;
+      s.x = p;
+      s.q = q;
+      GADI_TRY(launch_pw(c, s));
+      CsrUpdate<ST, 0> u;
+      u.st = c->hst;
+      u.p = p;
+      u.q = q;
+      u.u = (ST*)c->Z;
+      u.r = (ST*)c->R;
+      return launch_pw(c, u);
+    });
+  }
+  static int s_solve_csr(Ctx* c, double coeff, double tol, int maxit) {
+    CsrCgnrRhs<ST> rh;
+    rh.z = (const ST*)c->Z;
+    rh.r = (ST*)c->R;
+    rh.y = (ST*)c->Y;
+    rh.coeff = (CT)coeff;
+    GADI_TRY(launch_pw(c, rh));
+    const CsrT<ST> S = csr_s(c, CS_S), STm = csr_s(c, CS_ST);
+    CsrSpmv<ST, 3> in;
+    in.st = c->sst;
+    in.m = STm;
+    in.x = (const ST*)c->R;
+    in.q = (ST*)c->RB;
+    in.tol = tol;
+    in.maxit = maxit;
+    GADI_TRY(launch_pw(c, in));
+    ST* p = (ST*)c->P[0];
+    ST* w = (ST*)c->P[1];
+    return run_batched(c, c->sst, c->h_sst, c->pred_s, maxit, [&](int k) {
+      CsrDir<ST> d;
+      d.st = c->sst;
+      d.f = (const ST*)c->RB;
+      d.p = p;
+      d.first = k == 0;
+      GADI_TRY(launch_pw(c, d));
+      CsrSpmv<ST, 1> s;
+      s.st = c->sst;
+      s.m = S;
+      s.x = p;
+      s.q = w;
+      GADI_TRY(launch_pw(c, s));
+      CsrUpdate<ST, 1> u;
+      u.st = c->sst;
+      u.p = p;
+      u.q = w;
+      u.u = (ST*)c->Y;
+      u.r = (ST*)c->R;
+      GADI_TRY(launch_pw(c, u));
+      CsrSpmv<ST, 2> t;
+      t.st = c->sst;
+      t.m = STm;
+      t.x = (const ST*)c->R;
+      t.q = (ST*)c->RB;
+      return launch_pw(c, t);
+    });
+  }
+  template <int UR, bool HAS_E>
+  static int outer_csr_t(Ctx* c, double scale) {
+    CsrOuterX<ST> ox;
+    ox.x = c->x[c->xcur];
+    ox.y = (const ST*)c->Y;
+    ox.xout = c->x[c->xcur ^ 1];
+    ox.scale = scale;
+    ox.u32 = (c->u != GADI_FP64 && c->u != GADI_FP64X2) ? 1 : 0;
+    GADI_TRY(launch_pw(c, ox));
+    CsrOuterR<UR, HAS_E> o;
+    o.A = csr_d(c, CS_A);
+    o.x = c->x[c->xcur ^ 1];
+    o.xs = c->xs;
+    o.b = c->b;
+    o.r = c->r;
+    o.out = c->osum;
+    o.ones = c->ones;
+    GADI_TRY(launch_pw(c, o));
+    c->xcur ^= 1;
+    return 0;
+  }
+  static int outer_csr(Ctx* c, double scale, int has_e) {
+    const int ur = c->ur == GADI_FP64 ? 0 : (c->ur == GADI_FP64X2 ? 2 : 1);
+    if (ur == 0) return has_e ? outer_csr_t<0, true>(c, scale) : outer_csr_t<0, false>(c, scale);
+    if (ur == 1) return has_e ? outer_csr_t<1, true>(c, scale) : outer_csr_t<1, false>(c, scale);
+    return has_e ? outer_csr_t<2, true>(c, scale) : outer_csr_t<2, false>(c, scale);
+  }
+  static int apply_csr(Ctx* c, int op, int strict, const double* in, double* out) {
+    const int slot = op == 1 ? CS_H : (op == 2 ? CS_S : CS_ST);
+    if (strict) {
+      CsrApply<ST, true> a;
+      a.m = csr_d(c, slot);
+      a.in = in;
+      a.outv = out;
+      return launch_pw(c, a);
+    }
+    CsrApply<ST, false> a;
+    a.m = csr_d(c, slot);
+    a.in = in;
+    a.outv = out;
+    return launch_pw(c, a);
+  }
 
   // ------------------------------------------------------------ H-solve (CG)
   template <int DIM, int ZS>
@@ -363,21 +515,25 @@ struct Engine {
 
   // ------------------------------------------------------------ vtable
   static int h_solve(Ctx* c, double scale, double tol, int maxit) {
+    if (c->kind == GADI_CSR) return h_solve_csr(c, scale, tol, maxit);
     if (c->kind == GADI_COMPLEX) return h_solve_t<2, 2>(c, scale, tol, maxit);
     if (c->ndim == 3) return h_solve_t<3, 1>(c, scale, tol, maxit);
     return h_solve_t<2, 1>(c, scale, tol, maxit);
   }
   static int s_solve(Ctx* c, double coeff, double tol, int maxit) {
+    if (c->kind == GADI_CSR) return s_solve_csr(c, coeff, tol, maxit);
     if (c->kind == GADI_COMPLEX) return s_solve_cplx(c, coeff, tol, maxit);
     if (c->ndim == 3) return s_solve_real<3>(c, coeff, tol, maxit);
     return s_solve_real<2>(c, coeff, tol, maxit);
   }
   static int outer(Ctx* c, double scale, int has_e) {
+    if (c->kind == GADI_CSR) return outer_csr(c, scale, has_e);
     if (c->kind == GADI_COMPLEX) return outer_d<2, 2, true>(c, scale, has_e);
     if (c->ndim == 3) return outer_d<3, 1, false>(c, scale, has_e);
     return outer_d<2, 1, false>(c, scale, has_e);
   }
   static int apply(Ctx* c, int op, int strict, const double* in, double* out) {
+    if (c->kind == GADI_CSR) return apply_csr(c, op, strict, in, out);
     const CoefT<double>& C = op == 1 ? c->H : (op == 2 ? c->S : c->ST);
     if (c->kind == GADI_COMPLEX) {
       if (op == 1)

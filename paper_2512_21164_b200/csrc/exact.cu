@@ -42,6 +42,10 @@ struct XOp {
   int cplx, which;  // which: 1 H, 2 S, 3 S^T (crd only)
   double alpha;     // u_s image of alpha (crd S diagonal)
   const double* v;  // crd potential (fp64, per grid point)
+  // general CSR operator (kind GADI_CSR): values are the u_s images
+  const long long* rp;
+  const int* ci;
+  const double* cv;
 };
 
 // Row sum in ascending column order: first product, then q(acc + prod)
@@ -60,7 +64,9 @@ struct RowAcc {
 __global__ void xspmv_kernel(XOp op, const double* __restrict__ in, double* __restrict__ out, long long n, int f) {
   for (long long i = (long long)blockIdx.x * XT + threadIdx.x; i < n; i += (long long)gridDim.x * XT) {
     RowAcc r{0.0, false, f};
-    if (!op.cplx) {
+    if (op.rp) {
+      for (long long k = op.rp[i]; k < op.rp[i + 1]; ++k) r.add(op.cv[k], in[op.ci[k]]);
+    } else if (!op.cplx) {
       const long long plane = (long long)op.ny * op.nz;
       const long long x = i / plane, rem = i % plane;
       const int y = (int)(rem / op.nz), z = (int)(rem % op.nz);
@@ -215,6 +221,15 @@ XOp make_op(const Ctx* c, int which) {
   o.which = which;
   o.alpha = c->d.alpha_s;
   o.v = c->v64;
+  o.rp = nullptr;
+  o.ci = nullptr;
+  o.cv = nullptr;
+  if (c->kind == GADI_CSR) {
+    const CsrDev& m = c->csr[which == 1 ? CS_H : (which == 2 ? CS_S : CS_ST)];
+    o.rp = m.rp;
+    o.ci = m.ci;
+    o.cv = m.v64;
+  }
   return o;
 }
 

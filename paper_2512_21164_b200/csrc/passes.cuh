@@ -29,13 +29,19 @@ template <> struct CTOf<double> { typedef double type; };
 // Geometry traits.  DIM: 2 -> rows of 64 lanes, 1 row per CTA (the slow axis
 // is marched); 3 -> 32 lanes x 8 rows.  VZ elements per lane = one 16-byte
 // vector of the storage type (2 for fp64).
+#ifndef GADI_BY3
+#define GADI_BY3 8  // rows per 3-D tile (y-halo overhead (TY + 2) / TY)
+#endif
+#ifndef GADI_VZ64
+#define GADI_VZ64 2  // fp64 elements per lane (row width of an fp64 tile = 32 * VZ)
+#endif
 template <class ST_, int DIM, int ZS_>
 struct GeoT {
   typedef ST_ ST;
   typedef typename CTOf<ST_>::type CT;
-  static constexpr int VZ = (int)(16 / sizeof(ST_)) >= 2 ? (int)(16 / sizeof(ST_)) : 2;
+  static constexpr int VZ = sizeof(ST_) == 8 ? GADI_VZ64 : (int)(16 / sizeof(ST_));
   static constexpr int BZ = DIM == 3 ? 32 : 64;
-  static constexpr int BY = DIM == 3 ? 8 : 1;
+  static constexpr int BY = DIM == 3 ? GADI_BY3 : 1;
   static constexpr int ZS = ZS_;
   static constexpr int NT = BZ * BY;
 #ifndef GADI_TMA_MINB
@@ -64,6 +70,105 @@ struct NormState {
   double nw, sigma, tol, pad;
   int it, maxit, done, pad2;
 };
+
+// ---------------------------------------------------------------- scalar recurrences
+// The device-side scalar logic of the inner solvers, shared by the stencil
+// passes below, the CSR passes (csr.cuh) and the slab finalize kernel.
+// cg_spd (inner.py:67-86):
+__device__ __forceinline__ void fin_cg_alpha(InnerState* st, double php) {
+  if (php <= 0.0) {  // inner.py:70-72 breakdown
+    st->breakdown = 1;
+    st->done = 1;
+    return;
+  }
+  st->alpha = st->rs / php;
+}
+__device__ __forceinline__ void fin_cg_beta(InnerState* st, double rs_new) {
+  const int it = st->it + 1;
+  st->it = it;
+  const double relres = sqrt(fmax(rs_new, 0.0)) / st->nrhs;  // inner.py:78
+  st->relres = relres;
+  if (relres <= st->tol) {
+    st->converged = 1;
+    st->done = 1;
+    return;
+  }
+  if (rs_new <= 0.0) {  // inner.py:82-83
+    st->done = 1;
+    return;
+  }
+  st->beta = rs_new / st->rs;
+  st->rs = rs_new;
+  if (it >= st->maxit) st->done = 1;
+}
+// cg_normal_skew (inner.py:108-140):
+__device__ __forceinline__ void fin_cgnr_init(InnerState* st, double rs, double rhs2, double tol, int maxit) {
+  st->tol = tol;
+  st->maxit = maxit;
+  st->it = 0;
+  st->breakdown = 0;
+  st->converged = 0;
+  st->done = 0;
+  st->beta = 0.0;
+  st->relres = 1.0;
+  const double nrhs = sqrt(rhs2);
+  st->nrhs = nrhs;
+  st->rs = rs;
+  if (nrhs == 0.0) {  // zero right-hand side
+    st->converged = 1;
+    st->relres = 0.0;
+    st->done = 1;
+  } else if (maxit <= 0) {
+    st->done = 1;
+  }
+}
+__device__ __forceinline__ void fin_cgnr_alpha(InnerState* st, double denom) {
+  if (denom <= 0.0) {  // inner.py:123-125
+    st->breakdown = 1;
+    st->done = 1;
+    return;
+  }
+  st->alpha = st->rs / denom;
+}
+__device__ __forceinline__ void fin_cgnr_relres(InnerState* st, double rr) {
+  const int it = st->it + 1;
+  st->it = it;
+  const double relres = sqrt(rr) / st->nrhs;  // inner.py:130 (fp64 norm)
+  st->relres = relres;
+  if (relres <= st->tol) {
+    st->converged = 1;
+    st->done = 1;
+    return;
+  }
+  if (it >= st->maxit) st->done = 1;
+}
+__device__ __forceinline__ void fin_cgnr_beta(InnerState* st, double rs_new) {
+  if (rs_new <= 0.0) {  // inner.py:136-137
+    st->done = 1;
+    return;
+  }
+  st->beta = rs_new / st->rs;
+  st->rs = rs_new;
+}
+// matrix_norm_2 (analysis.py:58-69), after w = A^T A v and ||w||^2
+__device__ __forceinline__ void fin_norm(NormState* ns, double ww) {
+  const double nwn = sqrt(ww);
+  if (nwn == 0.0) {  // analysis.py:62-63
+    ns->sigma = 0.0;
+    ns->done = 1;
+    return;
+  }
+  const double sig_new = sqrt(nwn);
+  ns->nw = nwn;
+  ns->it += 1;
+  if (fabs(sig_new - ns->sigma) <= ns->tol * sig_new) {  // analysis.py:67-68
+    ns->sigma = sig_new;
+    ns->done = 1;
+    return;
+  }
+  ns->sigma = sig_new;
+  if (ns->it >= ns->maxit) ns->done = 1;
+}
 
 // Dot product of one lane's vector: products and partial sum in the compute
 // type, one fp64 accumulation per vector (cross-vector sums are fp64).
@@ -228,15 +333,7 @@ struct HcgA : G, PassBase {
     round_vec<ST>(s[0], hp);
     red[0] += dotv<CT, G::VZ>(fc[0], hp, nv);
   }
-  __device__ void finalize(const double (&t)[1]) const {
-    const double php = t[0];
-    if (php <= 0.0) {  // inner.py:70-72
-      st->breakdown = 1;
-      st->done = 1;
-      return;
-    }
-    st->alpha = st->rs / php;
-  }
+  __device__ void finalize(const double (&t)[1]) const { fin_cg_alpha(st, t[0]); }
 };
 
 // f = p ; Hp ; z += alpha p ; r -= alpha Hp ; sum r.r ; convergence, beta
@@ -296,25 +393,7 @@ struct HcgB : G, PassBase {
     store_any<ST, G::VZ>(z, i, nv, zn, g.vec);
     store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
   }
-  __device__ void finalize(const double (&t)[1]) const {
-    const double rs_new = t[0];
-    const int it = st->it + 1;
-    st->it = it;
-    const double relres = sqrt(fmax(rs_new, 0.0)) / st->nrhs;  // inner.py:78
-    st->relres = relres;
-    if (relres <= st->tol) {
-      st->converged = 1;
-      st->done = 1;
-      return;
-    }
-    if (rs_new <= 0.0) {  // inner.py:82-83
-      st->done = 1;
-      return;
-    }
-    st->beta = rs_new / st->rs;
-    st->rs = rs_new;
-    if (it >= st->maxit) st->done = 1;
-  }
+  __device__ void finalize(const double (&t)[1]) const { fin_cg_beta(st, t[0]); }
 };
 
 // ============================================================== CGNR passes
@@ -374,26 +453,7 @@ struct CgnrInit : G, PassBase {
     store_any<ST, G::VZ>(rbar, i, nv, rb, g.vec);
     store_any<ST, G::VZ>(y, i, nv, zero, g.vec);
   }
-  __device__ void finalize(const double (&t)[2]) const {
-    st->tol = tol;
-    st->maxit = maxit;
-    st->it = 0;
-    st->breakdown = 0;
-    st->converged = 0;
-    st->done = 0;
-    st->beta = 0.0;
-    st->relres = 1.0;
-    const double nrhs = sqrt(t[1]);
-    st->nrhs = nrhs;
-    st->rs = t[0];
-    if (nrhs == 0.0) {  // inner.py:119-120 zero right-hand side
-      st->converged = 1;
-      st->relres = 0.0;
-      st->done = 1;
-    } else if (maxit <= 0) {
-      st->done = 1;
-    }
-  }
+  __device__ void finalize(const double (&t)[2]) const { fin_cgnr_init(st, t[0], t[1], tol, maxit); }
 };
 
 // f = (it==0) ? rbar : round(rbar + beta p_in) ; w = S f ; store p_out ; sum w.w
@@ -466,15 +526,7 @@ struct CgnrP1 : G, PassBase {
     round_vec<ST>(s[0], w);
     red[0] += dotv<CT, G::VZ>(w, w, nv);
   }
-  __device__ void finalize(const double (&t)[1]) const {
-    const double denom = t[0];
-    if (denom <= 0.0) {  // inner.py:123-125
-      st->breakdown = 1;
-      st->done = 1;
-      return;
-    }
-    st->alpha = st->rs / denom;
-  }
+  __device__ void finalize(const double (&t)[1]) const { fin_cgnr_alpha(st, t[0]); }
 };
 
 // f = p ; w = S p ; y += alpha p ; r -= alpha w ; fp64 ||r||^2 ; convergence
@@ -536,18 +588,7 @@ struct CgnrP2 : G, PassBase {
     store_any<ST, G::VZ>(y, i, nv, yn, g.vec);
     store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
   }
-  __device__ void finalize(const double (&t)[1]) const {
-    const int it = st->it + 1;
-    st->it = it;
-    const double relres = sqrt(t[0]) / st->nrhs;  // inner.py:130 (fp64 norm)
-    st->relres = relres;
-    if (relres <= st->tol) {
-      st->converged = 1;
-      st->done = 1;
-      return;
-    }
-    if (it >= st->maxit) st->done = 1;
-  }
+  __device__ void finalize(const double (&t)[1]) const { fin_cgnr_relres(st, t[0]); }
 };
 
 // rbar = round(S^T r) ; rs_new = rbar.rbar ; beta
@@ -595,15 +636,7 @@ struct CgnrP3 : G, PassBase {
     red[0] += dotv<CT, G::VZ>(rb, rb, nv);
     store_any<ST, G::VZ>(rbar, i, nv, rb, g.vec);
   }
-  __device__ void finalize(const double (&t)[1]) const {
-    const double rs_new = t[0];
-    if (rs_new <= 0.0) {  // inner.py:136-137
-      st->done = 1;
-      return;
-    }
-    st->beta = rs_new / st->rs;
-    st->rs = rs_new;
-  }
+  __device__ void finalize(const double (&t)[1]) const { fin_cgnr_beta(st, t[0]); }
 };
 
 // ============================================================== outer pass
@@ -841,24 +874,7 @@ struct NormPass : G, PassBase {
     }
     store_any<double, VZ>(outv, i, nv, o, g.vec);
   }
-  __device__ void finalize(const double (&t)[1]) const {
-    const double nwn = sqrt(t[0]);
-    if (nwn == 0.0) {  // analysis.py:62-63
-      ns->sigma = 0.0;
-      ns->done = 1;
-      return;
-    }
-    const double sig_new = sqrt(nwn);
-    ns->nw = nwn;
-    ns->it += 1;
-    if (fabs(sig_new - ns->sigma) <= ns->tol * sig_new) {  // analysis.py:67-68
-      ns->sigma = sig_new;
-      ns->done = 1;
-      return;
-    }
-    ns->sigma = sig_new;
-    if (ns->it >= ns->maxit) ns->done = 1;
-  }
+  __device__ void finalize(const double (&t)[1]) const { fin_norm(ns, t[0]); }
 };
 
 // ============================================================== y = Op x

@@ -210,6 +210,20 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
     int gs = 0;
     while (it.next(tile, xa, xb)) {
       const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+      // Row spans clipped to the grid row [0, nz): the 16-byte pads and the
+      // part of a last partial tile past nz are never read by the consumers,
+      // and at a row boundary they would pull extra DRAM lines.  zt0, nz and
+      // the pads are 16-byte multiples on this path, so clipped copies stay
+      // aligned.  Input rows start at element zt0 - hz (smem offset 0).
+      int in_bytes[NIN > 0 ? NIN : 1];
+#pragma unroll
+      for (int j = 0; j < NIN; ++j) {
+        const int esz = P::in_esz(j), hz = TS::hz(esz);
+        in_bytes[j] = (min(zt0 + TZ + hz, g.nz) - max(zt0 - hz, 0)) * esz;
+      }
+      int epi_bytes[NE > 0 ? NE : 1];
+#pragma unroll
+      for (int j = 0; j < NE; ++j) epi_bytes[j] = (min(zt0 + TZ, g.nz) - zt0) * P::epi_esz(j);
       for (int xp = xa - 1; xp <= xb; ++xp, ++gs) {
         const int st = gs % NST;
         if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
@@ -223,13 +237,13 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
             if (p.in_active(j))
               for (int r = 0; r < TY + 2; ++r) {
                 const int yy = y0 - 1 + r;
-                if (yy >= 0 && yy < g.ny) bytes += TS::rb_in(j);
+                if (yy >= 0 && yy < g.ny) bytes += in_bytes[j];
               }
           if (ev) {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
               for (int r = 0; r < TY; ++r)
-                if (y0 + r < g.ny) bytes += TS::rb_epi(j);
+                if (y0 + r < g.ny) bytes += epi_bytes[j];
           }
         }
         if (lane == 0) mbar_expect_tx(&full[st], bytes);
@@ -241,9 +255,11 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
               const int yy = y0 - 1 + r;
               if (!p.in_active(j) || yy < 0 || yy >= g.ny) continue;
               const int esz = P::in_esz(j), hz = TS::hz(esz);
+              const int a = max(zt0 - hz, 0), b = min(zt0 + TZ + hz, g.nz);  // = in_e0 / in_bytes (j is runtime here)
               const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
-              const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0 - hz;
-              bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j), base + e0 * esz, (unsigned)TS::rb_in(j), &full[st]);
+              const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + a;
+              bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j) + (a - (zt0 - hz)) * esz, base + e0 * esz,
+                       (unsigned)((b - a) * esz), &full[st]);
             } else if (ev) {
               const int q2 = q - NIN * (TY + 2);
               const int j = q2 / TY, r = q2 % TY;
@@ -252,8 +268,8 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
               const int esz = P::epi_esz(j);
               const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
               const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0;
-              bulk_g2s(sb + TS::off_epi(j) + r * TS::rb_epi(j), base + e0 * esz, (unsigned)TS::rb_epi(j),
-                       &full[st]);
+              bulk_g2s(sb + TS::off_epi(j) + r * TS::rb_epi(j), base + e0 * esz,
+                       (unsigned)((min(zt0 + TZ, g.nz) - zt0) * esz), &full[st]);
             }
           }
         }

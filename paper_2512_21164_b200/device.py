@@ -54,6 +54,40 @@ def make_desc(spec: StencilSpec, alpha: float, u_s, u="fp64", u_r="fp64", *,
     return d
 
 
+def _csr(m, keep):
+    c = _lib.Csr()
+    ro = np.ascontiguousarray(m.row_offsets, dtype=np.int64)
+    ci = np.ascontiguousarray(m.col_indices, dtype=np.int64)
+    va = np.ascontiguousarray(m.values, dtype=np.float64)
+    keep += [ro, ci, va]
+    c.nrows, c.nnz = int(m.nrows), int(va.size)
+    c.row_offsets = ro.ctypes.data_as(C.POINTER(C.c_int64))
+    c.col_indices = ci.ctypes.data_as(C.POINTER(C.c_int64))
+    c.values = va.ctypes.data_as(C.POINTER(C.c_double))
+    return c
+
+
+def make_csr_desc(A, H, S, ST, u_s, u="fp64", u_r="fp64"):
+    """Descriptor of a general-CSR problem (csrc/csr.cuh): A in fp64 and the
+    splitting operators H_low, S_low, S_low_T with their u_s values."""
+    d = _lib.ProblemDesc()
+    d.kind = _lib.KIND_CSR
+    d.ndim = 1
+    d.dims[0], d.dims[1], d.dims[2] = int(A.nrows), 1, 1
+    d.n = int(A.nrows)
+    keep = []
+    d.csr_A, d.csr_H, d.csr_S, d.csr_ST = (_csr(m, keep) for m in (A, H, S, ST))
+    d.u = _lib.FMT_CODES[resolve_format(u).name]
+    d.u_r = _lib.FMT_CODES[resolve_format(u_r).name]
+    d.u_s = _lib.FMT_CODES[resolve_format(u_s).name]
+    d._keep = keep  # noqa: SLF001
+    return d
+
+
+def is_csr(a) -> bool:
+    return not isinstance(a, StencilMatrix) and hasattr(a, "row_offsets")
+
+
 def open_context(desc, device: int = 0, comm=None, slab=None) -> _lib.Context:
     return _lib.Context(desc, device, comm=comm, slab=slab)
 
@@ -81,8 +115,7 @@ def clear_cache():
 
 def _require_stencil(a):
     if not isinstance(a, StencilMatrix):
-        raise NotImplementedError(
-            "general CSR operators are served by the CSR engine (not available in this build)")
+        raise NotImplementedError(f"unsupported operator type {type(a).__name__}")
     return a
 
 
@@ -99,8 +132,14 @@ def _op_context(a: StencilMatrix, fmt):
 
 
 def spmv(a, x, fmt):
-    a = _require_stencil(a)
     fmt = resolve_format(fmt)
+    if is_csr(a):
+        if fmt.compensated:
+            raise NotImplementedError("fp64x2 spmv is provided through residual(..., 'fp64x2')")
+        us = fmt if fmt.significand_bits < 53 else resolve_format("fp64")
+        with open_context(make_csr_desc(a, a, a, a, us)) as ctx:
+            return ctx.spmv(0, x) if fmt.significand_bits >= 53 else ctx.spmv(1, x, strict=True)
+    a = _require_stencil(a)
     if fmt.compensated:
         raise NotImplementedError("fp64x2 spmv is provided through residual(..., 'fp64x2')")
     with _op_context(a, fmt) as ctx:
@@ -117,6 +156,11 @@ def spmv(a, x, fmt):
 
 
 def residual(a, x, b, fmt):
+    if is_csr(a):
+        fmt = resolve_format(fmt)
+        with open_context(make_csr_desc(a, a, a, a, "fp64", u="fp64", u_r=fmt)) as ctx:
+            ctx.set_rhs(b)
+            return ctx.residual(x)
     a = _require_stencil(a)
     if a.role != "A":
         raise NotImplementedError("residual is defined for the system matrix A")

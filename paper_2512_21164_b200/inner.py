@@ -15,7 +15,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .device import make_desc, open_context
+from .device import is_csr, make_csr_desc, make_desc, open_context
+from .sparsemat import transpose
 from .precision import resolve_format
 from .stencil import StencilMatrix
 
@@ -48,9 +49,13 @@ class InnerSolveStats:
     true_relative_residual: float = float("nan")
 
 
-def _ctx_for(op: StencilMatrix, fmt, which: str):
+def _ctx_for(op, fmt, which: str, op_t=None):
+    if is_csr(op):
+        # the operator sits in the H slot (CG) or the S / S^T slots (CGNR)
+        st = op_t if op_t is not None else (transpose(op) if which == "S" else op)
+        return open_context(make_csr_desc(op, op, op, st, fmt))
     if not isinstance(op, StencilMatrix):
-        raise NotImplementedError("general CSR operators are served by the CSR engine")
+        raise NotImplementedError(f"unsupported operator type {type(op).__name__}")
     spec = op.spec
     if spec.family == "crd":
         return open_context(make_desc(spec, op.alpha, fmt, coef_fmt=op.fmt))
@@ -58,9 +63,13 @@ def _ctx_for(op: StencilMatrix, fmt, which: str):
     return open_context(make_desc(spec, 0.0, fmt, H=c, S=c))
 
 
-def _true_relres(op: StencilMatrix, rhs, x, nrhs) -> float:
+def _true_relres(op, rhs, x, nrhs) -> float:
     if nrhs == 0.0:
         return 0.0
+    if is_csr(op):  # fp64 true residual (inner.py:88, 142)
+        with open_context(make_csr_desc(op, op, op, op, "fp64")) as ctx:
+            y = ctx.spmv(0, x)
+        return float(np.linalg.norm(rhs - y)) / nrhs
     spec = op.spec
     if spec.family == "crd":
         ctx = open_context(make_desc(spec, op.alpha, "fp64", coef_fmt=op.fmt))
@@ -98,7 +107,7 @@ def cg_normal_skew(s, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt
     rhs = np.asarray(rhs, dtype=np.float64)
     if maxit is None:
         maxit = default_maxit(rhs.size)
-    with _ctx_for(s, fmt, "S") as ctx:
+    with _ctx_for(s, fmt, "S", s_transpose) as ctx:
         ctx.set_rounding(1 if rounding == "reference" else 0, dot_format(fmt, strict_model).name)
         y, st = ctx.s_solve(rhs, tol, maxit)
     nrhs = float(np.linalg.norm(rhs))

@@ -157,10 +157,66 @@ def inner_cases():
     return out
 
 
+def csr_cases(out):
+    """General sparse systems (the reference's own graded / mixed families,
+    TST/conftest.py:15-53, built by importing that conftest) for the CSR
+    engine: matrices, kernel outputs and solve histories (c4, c5 settings,
+    TST/test_acceptance.py:121-158)."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import graded_problem, mixed_problem  # noqa: E402
+
+    arrays, res = {}, []
+    problems = {"graded1e2": graded_problem(50, 1e2), "graded1e4": graded_problem(50, 1e4),
+                "graded1e6": graded_problem(50, 1e6), "mixed1e6": mixed_problem(50, 1e6)}
+    rng = np.random.default_rng(99)
+    for tag, p in problems.items():
+        a = p.A
+        arrays[f"{tag}/rp"], arrays[f"{tag}/ci"], arrays[f"{tag}/v"] = a.row_offsets, a.col_indices, a.values
+        arrays[f"{tag}/b"], arrays[f"{tag}/xs"] = p.b, p.exact_solution
+        x = rng.standard_normal(a.nrows)
+        b = rng.standard_normal(a.nrows)
+        arrays[f"{tag}/x"], arrays[f"{tag}/bvec"] = x, b
+        arrays[f"{tag}/res_fp64"] = residual(a, x, b, "fp64")
+        xq32 = quantize(x, "fp32")
+        arrays[f"{tag}/xq32"] = xq32
+        arrays[f"{tag}/res_fp32"] = residual(a.quantized("fp32"), xq32, quantize(b, "fp32"), "fp32")
+        arrays[f"{tag}/res_fp64x2"] = residual(a, x, b, "fp64x2")
+        arrays[f"{tag}/Ax_fp64"] = spmv(a, x, "fp64")
+        arrays[f"{tag}/norm2"] = np.array([matrix_norm_2(a)])
+        for us in ("bf16", "fp32"):
+            sp = make_hss_splitting(a, 1.0, us)
+            xq = quantize(x, us)
+            arrays[f"{tag}/{us}/xq"] = xq
+            for nm, m in (("H", sp.H_low), ("S", sp.S_low), ("ST", sp.S_low_T)):
+                arrays[f"{tag}/{us}/{nm}"] = spmv(m, xq, us)
+    runs = []
+    for tag in ("graded1e2", "graded1e4", "graded1e6"):
+        for us in ("bf16", "fp32"):
+            runs.append((f"c4_{tag}_{us}", tag, {"alpha": 1.0, "u_s": us, "outer_tol": 0.0, "outer_maxit": 600,
+                                                 "inner_tol": 1e-4}))
+    for ur in ("fp32", "fp64x2"):
+        runs.append((f"c5_mixed1e6_{ur}", "mixed1e6", {"alpha": 1.0, "u": "fp32", "u_r": ur, "u_s": "fp32",
+                                                       "outer_tol": 0.0, "outer_maxit": 600, "inner_tol": 1e-4}))
+    runs.append(("conv_graded1e4_bf16", "graded1e4", {"alpha": 1.0, "u_s": "bf16", "outer_tol": 1e-10}))
+    runs.append(("conv_mixed1e6_fp64", "mixed1e6", {"alpha": 1.0, "u_s": "fp64", "outer_tol": 1e-10}))
+    for name, tag, cfg in runs:
+        t0 = time.perf_counter()
+        rep = gadi_solve(problems[tag], cfg=GadiConfig(**cfg))
+        h = rep.history
+        res.append({"name": name, "problem": tag, "cfg": cfg, "status": rep.status, "outer": rep.iterations,
+                    "inner_h": [r.inner_h_iterations for r in h], "inner_s": [r.inner_s_iterations for r in h],
+                    "relres": [r.relative_residual for r in h], "berr": [r.backward_error for r in h],
+                    "ferr": [r.forward_error for r in h], "norm_A": rep.norm_A, "x_head": rep.x[:8].tolist(),
+                    "wall_s": time.perf_counter() - t0})
+        print(f"{name}: {rep.status} outer={rep.iterations} berr={h[-1].backward_error:.3e}", flush=True)
+    np.savez_compressed(out / "csr.npz", **arrays)
+    (out / "csr.json").write_text(json.dumps(res))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--only", choices=["kernels", "solves", "inner"], default=None)
+    ap.add_argument("--only", choices=["kernels", "solves", "inner", "csr"], default=None)
     a = ap.parse_args()
     HERE.mkdir(parents=True, exist_ok=True)
     if a.only in (None, "kernels"):
@@ -169,6 +225,9 @@ def main():
     if a.only in (None, "inner"):
         (HERE / "inner.json").write_text(json.dumps(inner_cases()))
         print("inner done", flush=True)
+    if a.only in (None, "csr"):
+        csr_cases(HERE)
+        print("csr done", flush=True)
     if a.only in (None, "solves"):
         res = []
         for c in solve_cases(a.quick):

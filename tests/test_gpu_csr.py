@@ -1,0 +1,114 @@
+"""General-CSR engine (csrc/csr.cuh) against the reference on its own sparse
+test families (graded / mixed block systems, TST/conftest.py:15-53; c4 and c5
+settings of TST/test_acceptance.py:121-158).  Fixtures: tests/golden/csr.*,
+made by tests/golden/make_golden.py --only csr from the unmodified reference.
+
+* kernels: fp64 / fp32-emulated / compensated residuals, A x and the strict
+  u_s SpMV on H_low, S_low, S_low_T -- bitwise; ||A||_2 to 1e-12;
+* solves, storage model: status, outer count +-1 (stagnation runs: the window
+  test, as in test_gpu_solve), final berr within 2x; the c4 / c5 acceptance
+  properties themselves (berr floor bound and spread, >= 10x forward-error
+  gain of the compensated residual);
+* solves, rounding="reference": outer and inner counts exactly."""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2512_21164_b200 as g
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def csr_golden():
+    return np.load(GOLDEN / "csr.npz"), {c["name"]: c for c in json.loads((GOLDEN / "csr.json").read_text())}
+
+
+def _matrix(arr, tag):
+    n = arr[f"{tag}/rp"].size - 1
+    return g.SparseMatrix(arr[f"{tag}/rp"], arr[f"{tag}/ci"], arr[f"{tag}/v"], (n, n))
+
+
+def _problem(arr, tag):
+    return g.Problem(A=_matrix(arr, tag), b=arr[f"{tag}/b"], exact_solution=arr[f"{tag}/xs"], label=tag)
+
+
+def _bits(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    bad = (a.view(np.uint64) != b.view(np.uint64)) & ~((a == 0) & (b == 0))
+    return not bad.any()
+
+
+TAGS = ["graded1e2", "graded1e4", "graded1e6", "mixed1e6"]
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_csr_kernels_bitwise(gpu, csr_golden, tag):
+    arr, _ = csr_golden
+    a = _matrix(arr, tag)
+    x, b = arr[f"{tag}/x"], arr[f"{tag}/bvec"]
+    assert _bits(g.residual(a, x, b, "fp64"), arr[f"{tag}/res_fp64"])
+    assert _bits(g.spmv(a, x, "fp64"), arr[f"{tag}/Ax_fp64"])
+    assert _bits(g.residual(a.quantized("fp32"), arr[f"{tag}/xq32"], g.quantize(b, "fp32"), "fp32"),
+                 arr[f"{tag}/res_fp32"])
+    assert _bits(g.residual(a, x, b, "fp64x2"), arr[f"{tag}/res_fp64x2"])
+    assert g.matrix_norm_2(a) == pytest.approx(float(arr[f"{tag}/norm2"][0]), rel=1e-12)
+    for us in ("bf16", "fp32"):
+        sp = g.make_hss_splitting(a, 1.0, us)
+        xq = arr[f"{tag}/{us}/xq"]
+        for nm, m in (("H", sp.H_low), ("S", sp.S_low), ("ST", sp.S_low_T)):
+            assert _bits(g.spmv(m, xq, us), arr[f"{tag}/{us}/{nm}"]), (us, nm)
+
+
+NAMES = ["c4_graded1e2_bf16", "c4_graded1e2_fp32", "c4_graded1e4_bf16", "c4_graded1e4_fp32",
+         "c4_graded1e6_bf16", "c4_graded1e6_fp32", "c5_mixed1e6_fp32", "c5_mixed1e6_fp64x2",
+         "conv_graded1e4_bf16", "conv_mixed1e6_fp64"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_csr_solve_matches_reference(gpu, csr_golden, name):
+    arr, runs = csr_golden
+    c = runs[name]
+    rep = g.gadi_solve(_problem(arr, c["problem"]), cfg=g.GadiConfig(**c["cfg"]))
+    assert rep.status == c["status"], (rep.status, c["status"])
+    if c["status"] == "Stagnated":
+        assert abs(rep.iterations - c["outer"]) <= max(10, int(0.1 * c["outer"]))
+    else:
+        assert abs(rep.iterations - c["outer"]) <= 1, (rep.iterations, c["outer"])
+    b_got, b_ref = rep.history[-1].backward_error, c["berr"][-1]
+    assert 0.5 * b_ref <= b_got <= 2.0 * b_ref, (b_got, b_ref)
+    assert rep.norm_A == pytest.approx(c["norm_A"], rel=1e-10)
+
+
+def test_csr_acceptance_c4_c5(gpu, csr_golden):
+    """The reference's acceptance properties on the GPU runs themselves."""
+    arr, runs = csr_golden
+    floors = []
+    for tag in ("graded1e2", "graded1e4", "graded1e6"):
+        for us in ("bf16", "fp32"):
+            rep = g.gadi_solve(_problem(arr, tag), cfg=g.GadiConfig(**runs[f"c4_{tag}_{us}"]["cfg"]))
+            floors.append(rep.history[-1].backward_error)
+    floors = np.array(floors)
+    assert floors.max() <= 1e3 * 100 * 2.0 ** -53          # TST/test_acceptance.py:133-138
+    assert floors.max() / floors.min() <= 10.0
+    errs = {}
+    for ur in ("fp32", "fp64x2"):
+        rep = g.gadi_solve(_problem(arr, "mixed1e6"), cfg=g.GadiConfig(**runs[f"c5_mixed1e6_{ur}"]["cfg"]))
+        errs[ur] = rep.history[-1].forward_error
+    assert errs["fp32"] / errs["fp64x2"] >= 10.0            # TST/test_acceptance.py:157-158
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_csr_solve_reference_rounding_exact(gpu, csr_golden, name):
+    arr, runs = csr_golden
+    c = runs[name]
+    rep = g.gadi_solve(_problem(arr, c["problem"]), cfg=g.GadiConfig(**c["cfg"]), rounding="reference")
+    assert rep.status == c["status"]
+    assert rep.iterations == c["outer"], (rep.iterations, c["outer"])
+    assert [h.inner_h_iterations for h in rep.history] == c["inner_h"]
+    assert [h.inner_s_iterations for h in rep.history] == c["inner_s"]
+    assert np.array_equal(rep.x[:8], np.array(c["x_head"]))
