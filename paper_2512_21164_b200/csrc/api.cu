@@ -7,6 +7,7 @@
 #include <cstring>
 #include <string>
 #include "engine.cuh"
+#include "norm_fused.cuh"
 
 namespace gadi {
 
@@ -89,9 +90,48 @@ static int norm_pass_d(Ctx* c, const double* in, double* out) {
     p.outv = out;
     return launch_pw(c, p);
   }
-  if (c->kind == GADI_COMPLEX) return norm_pass<2, 2, true, TRANS>(c, in, out);
+  if (c->kind == GADI_COMPLEX)
+    return c->ndim == 3 ? norm_pass<3, 2, true, TRANS>(c, in, out) : norm_pass<2, 2, true, TRANS>(c, in, out);
   if (c->ndim == 3) return norm_pass<3, 1, false, TRANS>(c, in, out);
   return norm_pass<2, 1, false, TRANS>(c, in, out);
+}
+
+// One power-iteration step in a single sweep (norm_fused.cuh): single-domain
+// real stencils whose rows are TMA-aligned; other contexts use the two passes.
+static bool norm_fused_ok(const Ctx* c) {
+  if (c->kind != GADI_STENCIL || c->comm || c->no_tma) return false;
+  if (getenv("GADI_NORM_2PASS") && atoi(getenv("GADI_NORM_2PASS"))) return false;
+  return ((long long)c->nz * 8) % 16 == 0 && c->nz % GADI_VZ64 == 0;
+}
+
+template <int DIM>
+static int norm_fused_step(Ctx* c, const double* in, double* out) {
+  using S = NFShape<DIM>;
+  NormFused<DIM> p;
+  p.defer = nullptr;
+  p.partials = c->partials;
+  p.ticket = c->ticket;
+  p.ns = c->nst;
+  p.in = in;
+  p.outv = out;
+  p.A = c->A;
+  p.AT = c->AT;
+  static int occ = 0;
+  if (!occ) {
+    GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, norm_fused_kernel<DIM>, S::NTOT, S::SMEM));
+    if (occ < 1) occ = 1;
+  }
+  p.g = make_geom(c, S::TZ, S::TY, S::VZ, (long long)occ * c->sms);
+  const long long units = (long long)p.g.nzt * p.g.nyt * p.g.nx;
+  const int nb = (int)std::min<long long>(units, (long long)occ * c->sms * c->waves);
+  if (nb > c->pstride) return set_error("fused norm grid exceeds partials buffer", GADI_ERR_ARG);
+  prof_begin(c, K_NORM_B);
+  norm_fused_kernel<DIM><<<nb, S::NTOT, S::SMEM, c->stream>>>(p);
+  prof_end(c);
+  c->launches++;
+  GADI_CUDA(cudaGetLastError());
+  return 0;
 }
 
 // Vectors carry guard bands so the TMA sweep may copy whole padded rows
@@ -270,10 +310,16 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
       return set_error("2-D stencils use dims (n_g, 1, n_g)", GADI_ERR_ARG);
     }
   } else {
+    // crd: interleaved (re, im) pairs, z-stride 2; 2-D (n_g, 1, n_g) or the
+    // 3-D extension (n_g, n_g, n_g)
     c->nx = (int)desc->dims[0];
-    c->ny = 1;
+    c->ny = (int)desc->dims[1];
     c->nz = 2 * (int)desc->dims[2];
-    c->ndim = 2;
+    c->ndim = desc->ndim == 3 ? 3 : 2;
+    if (c->ndim == 2 && c->ny != 1) {
+      delete h;
+      return set_error("2-D crd uses dims (n_g, 1, n_g)", GADI_ERR_ARG);
+    }
     if (c->ur != GADI_FP64) {
       delete h;
       return set_error("complex family supports u_r = fp64 only", GADI_ERR_UNSUPPORTED);
@@ -377,7 +423,7 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   CHK(cudaMemsetAsync(c->sst, 0, sizeof(InnerState), c->stream));
   if (c->kind == GADI_COMPLEX) {
     // desc->v is the whole grid's potential; this slab owns rows [x0, x0+nx)
-    const double* vs = desc->v + (size_t)c->x0 * (size_t)(c->nz / 2);
+    const double* vs = desc->v + (size_t)c->x0 * (size_t)c->ny * (size_t)(c->nz / 2);
     CHK(cudaMemcpyAsync(c->v64, vs, sizeof(double) * (size_t)(c->n / 2), cudaMemcpyHostToDevice, c->stream));
     int rc = c->vt->quantize(c, c->v64, c->VS, c->n / 2);
     if (rc) {
@@ -485,6 +531,7 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
   GADI_CUDA(cudaSetDevice(c->device));
   double* w = c->x[0];
   double* t = c->x[1];
+  const bool fused = norm_fused_ok(c);
   GADI_CUDA(cudaEventRecord(c->ev[6], c->stream));
   if (v0) {
     GADI_TRY(upload(c, v0, w));  // this slab's rows of the normalised start vector
@@ -510,6 +557,11 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
   while (launched < maxit) {
     const int nb = std::min(batch, maxit - launched);
     for (int j = 0; j < nb; ++j) {
+      if (fused) {
+        GADI_TRY(c->ndim == 3 ? norm_fused_step<3>(c, w, t) : norm_fused_step<2>(c, w, t));
+        std::swap(w, t);
+        continue;
+      }
       GADI_TRY(norm_pass_d<false>(c, w, t));
       GADI_TRY(halo(c, t, 8));
       GADI_TRY(norm_pass_d<true>(c, t, w));

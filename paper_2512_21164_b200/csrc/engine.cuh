@@ -516,7 +516,8 @@ struct Engine {
   // ------------------------------------------------------------ vtable
   static int h_solve(Ctx* c, double scale, double tol, int maxit) {
     if (c->kind == GADI_CSR) return h_solve_csr(c, scale, tol, maxit);
-    if (c->kind == GADI_COMPLEX) return h_solve_t<2, 2>(c, scale, tol, maxit);
+    if (c->kind == GADI_COMPLEX)
+      return c->ndim == 3 ? h_solve_t<3, 2>(c, scale, tol, maxit) : h_solve_t<2, 2>(c, scale, tol, maxit);
     if (c->ndim == 3) return h_solve_t<3, 1>(c, scale, tol, maxit);
     return h_solve_t<2, 1>(c, scale, tol, maxit);
   }
@@ -528,7 +529,8 @@ struct Engine {
   }
   static int outer(Ctx* c, double scale, int has_e) {
     if (c->kind == GADI_CSR) return outer_csr(c, scale, has_e);
-    if (c->kind == GADI_COMPLEX) return outer_d<2, 2, true>(c, scale, has_e);
+    if (c->kind == GADI_COMPLEX)
+      return c->ndim == 3 ? outer_d<3, 2, true>(c, scale, has_e) : outer_d<2, 2, true>(c, scale, has_e);
     if (c->ndim == 3) return outer_d<3, 1, false>(c, scale, has_e);
     return outer_d<2, 1, false>(c, scale, has_e);
   }
@@ -536,6 +538,8 @@ struct Engine {
     if (c->kind == GADI_CSR) return apply_csr(c, op, strict, in, out);
     const CoefT<double>& C = op == 1 ? c->H : (op == 2 ? c->S : c->ST);
     if (c->kind == GADI_COMPLEX) {
+      if (op == 1 && c->ndim == 3)
+        return strict ? apply_sweep<3, 2, true>(c, C, in, out) : apply_sweep<3, 2, false>(c, C, in, out);
       if (op == 1)
         return strict ? apply_sweep<2, 2, true>(c, C, in, out) : apply_sweep<2, 2, false>(c, C, in, out);
       if (op == 2) return strict ? apply_cplx<false, true>(c, in, out) : apply_cplx<false, false>(c, in, out);

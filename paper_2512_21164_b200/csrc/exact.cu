@@ -83,14 +83,17 @@ __global__ void xspmv_kernel(XOp op, const double* __restrict__ in, double* __re
       const int comp = (int)(i & 1);
       const int ng = op.nz / 2;
       if (op.which == 1) {
-        const long long gx = g / ng;
-        const int gz = (int)(g % ng);
+        const long long gplane = (long long)op.ny * ng;  // grid points per x-plane
+        const long long gx = g / gplane, grem = g % gplane;
+        const int gy = (int)(grem / ng), gz = (int)(grem % ng);
         const CoefT<double>& c = op.c;
-        if (c.lo[0] != 0.0 && gx > 0) r.add(c.lo[0], in[i - 2LL * ng]);
+        if (c.lo[0] != 0.0 && gx > 0) r.add(c.lo[0], in[i - 2LL * gplane]);
+        if (c.lo[1] != 0.0 && gy > 0) r.add(c.lo[1], in[i - 2LL * ng]);
         if (c.lo[2] != 0.0 && gz > 0) r.add(c.lo[2], in[i - 2]);
         if (c.d != 0.0) r.add(c.d, in[i]);
         if (c.up[2] != 0.0 && gz < ng - 1) r.add(c.up[2], in[i + 2]);
-        if (c.up[0] != 0.0 && gx < op.nx - 1) r.add(c.up[0], in[i + 2LL * ng]);
+        if (c.up[1] != 0.0 && gy < op.ny - 1) r.add(c.up[1], in[i + 2LL * ng]);
+        if (c.up[0] != 0.0 && gx < op.nx - 1) r.add(c.up[0], in[i + 2LL * gplane]);
       } else {
         // S:   re row: a x_re, then -v x_im ; im row: v x_re, then a x_im
         // S^T: re row: a x_re, then +v x_im ; im row: -v x_re, then a x_im

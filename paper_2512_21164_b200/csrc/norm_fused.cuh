@@ -1,0 +1,294 @@
+// One power-iteration step of ||A||_2 (analysis.py:58-66) in ONE sweep:
+//     v = w / ||w|| ;  t = A v ;  w' = A^T t ;  sum w'^2
+// The two-pass form (NormPass<false>, NormPass<true>) streams 4 fp64 vectors
+// per iteration (read w, write t, read t, write w'); this kernel streams 2.
+// t never leaves the SM: while the CTA marches along x it computes the
+// t-plane x+1 on its tile plus a one-cell ring (halo warps own the two
+// y-halo rows, the edge lanes the two z-halo columns) from the v-planes
+// x, x+1, x+2 held in the TMA stage ring, keeps t for its own columns in a
+// 3-plane register queue (x-neighbours) and the whole t-plane in a
+// triple-buffered shared-memory plane (y / z neighbours), and applies A^T to
+// produce w'-plane x.  Every t and w' value is computed with exactly the
+// operations of the two-pass form (v = w * (1/nw), ordered fp64 stencils in
+// ascending column order), so the result is bitwise the same.
+//
+// Real 5-point (DIM 2: rows of 64 lanes) and 7-point (DIM 3: 32 lanes x TY
+// rows) stencils on a single domain; the crd family and slab contexts keep
+// the two-pass form.
+#pragma once
+#include "sweep_tma.cuh"
+
+namespace gadi {
+
+template <int DIM>
+struct NFShape {
+  static constexpr int VZ = GADI_VZ64;
+  static constexpr int BZ = DIM == 3 ? 32 : 64;
+  static constexpr int TY = DIM == 3 ? GADI_BY3 : 1;
+  static constexpr int TZ = BZ * VZ;
+  static constexpr int HZ = 2;                       // 16-byte pad = 2 fp64 each side
+  static constexpr int HV = DIM == 3 ? 2 : 0;        // v halo rows each side
+  static constexpr int HT = DIM == 3 ? 1 : 0;        // t halo rows each side
+  static constexpr int VROWS = TY + 2 * HV;
+  static constexpr int ROW = TZ + 2 * HZ;            // elements per smem row (v and t)
+  static constexpr int STAGE = VROWS * ROW * 8;
+  static constexpr int TROWS = TY + 2 * HT;
+  static constexpr int TPLANE = TROWS * ROW;         // elements per t buffer
+  static constexpr int NT = BZ * TY;
+  static constexpr int NH = DIM == 3 ? 2 : 0;        // halo warps (one per t halo row)
+  static constexpr int NCONS = NT + 32 * NH;
+  static constexpr int NTOT = NCONS + 32;
+  static constexpr int TBYTES = 3 * TPLANE * 8;
+  static constexpr int BUDGET = 100 * 1024;
+  static constexpr int NST_RAW = (BUDGET - TBYTES) / STAGE;
+  static constexpr int NST = NST_RAW < 4 ? 4 : (NST_RAW > 10 ? 10 : NST_RAW);
+  static constexpr size_t SMEM = (size_t)TBYTES + (size_t)NST * STAGE + 2 * NST * sizeof(uint64_t);
+};
+
+template <int DIM>
+struct NormFused {
+  SweepGeom g;
+  double* defer;
+  double* partials;
+  unsigned int* ticket;
+  NormState* ns;
+  const double* in;  // w
+  double* outv;      // w'
+  CoefT<double> A, AT;
+  double rnw;
+  static constexpr int NR = 1;
+  static constexpr bool HAS_RED = true;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  __device__ bool prepare() {
+    if (ns->done) return false;
+    rnw = 1.0 / ns->nw;
+    return true;
+  }
+  __device__ void finalize(const double (&t)[1]) const { fin_norm(ns, t[0]); }
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(NFShape<DIM>::NTOT, 1) norm_fused_kernel(NormFused<DIM> p) {
+  using S = NFShape<DIM>;
+  constexpr int VZ = S::VZ, BZ = S::BZ, TY = S::TY, TZ = S::TZ, HZ = S::HZ, HV = S::HV, HT = S::HT;
+  constexpr int ROW = S::ROW, NST = S::NST, NT = S::NT, NCONS = S::NCONS, NWCONS = NCONS / 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* tbuf = reinterpret_cast<double*>(smem_raw);
+  unsigned char* stages = smem_raw + S::TBYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)NST * S::STAGE);
+  uint64_t* empty = full + NST;
+
+  if (!p.prepare()) return;
+  const SweepGeom g = p.g;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double red[1] = {0.0};
+
+  if (tid >= NCONS) {
+    // ---------------------------------------------------------------- producer
+    constexpr int NCOPY = S::VROWS;
+    SegIter it(g, gridDim.x, blockIdx.x);
+    int tile, xa, xb, gs = 0;
+    while (it.next(tile, xa, xb)) {
+      const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+      const int za = max(zt0 - HZ, 0), zbnd = min(zt0 + TZ + HZ, g.nz);
+      const unsigned rowbytes = (unsigned)((zbnd - za) * 8), dst0 = (unsigned)((za - (zt0 - HZ)) * 8);
+      for (int xp = xa - 2; xp <= xb + 1; ++xp, ++gs) {
+        const int st = gs % NST;
+        if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
+        unsigned char* sb = stages + (size_t)st * S::STAGE;
+        const bool pv = xp >= 0 && xp < g.nx;
+        unsigned bytes = 0;
+        if (pv)
+          for (int r = 0; r < NCOPY; ++r) {
+            const int yy = y0 - HV + r;
+            if (yy >= 0 && yy < g.ny) bytes += rowbytes;
+          }
+        if (lane == 0) mbar_expect_tx(&full[st], bytes);
+        __syncwarp();
+        if (pv)
+          for (int r = lane; r < NCOPY; r += 32) {
+            const int yy = y0 - HV + r;
+            if (yy < 0 || yy >= g.ny) continue;
+            const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + za;
+            bulk_g2s(sb + (size_t)r * ROW * 8 + dst0, p.in + e0, rowbytes, &full[st]);
+          }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- consumers
+    const bool halo = tid >= NT;
+    const int tz = halo ? lane : tid % BZ;
+    const int trow = halo ? ((tid - NT) / 32 == 0 ? 0 : TY + 2 * HT - 1) : tid / BZ + HT;  // row in the t buffer
+    const int vrow = trow - HT + HV;                                                           // same y in a v stage
+    const bool edge_l = !halo && tz == 0, edge_r = !halo && tz == BZ - 1;
+    const double rnw = p.rnw;
+    auto wait_full = [&](int s) { mbar_wait(&full[s % NST], (unsigned)((s / NST) & 1)); };
+    auto release = [&](int s) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s % NST]);
+    };
+    auto vrowp = [&](int s, int r) {
+      return reinterpret_cast<const double*>(stages + (size_t)(s % NST) * S::STAGE) + (size_t)r * ROW;
+    };
+
+    SegIter it(g, gridDim.x, blockIdx.x);
+    int tile, xa, xb, gs = 0;
+    while (it.next(tile, xa, xb)) {
+      const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+      const int y = y0 + trow - HT;
+      const bool yok = y >= 0 && y < g.ny;
+      const int zb = zt0 + tz * VZ;
+      const bool zok = zb < g.nz;          // nz % VZ == 0: a lane's vector is all in or all out
+      const bool own = yok && zok;
+      // validity of v rows y-1, y, y+1 and of the z-halo columns
+      const bool ym_ok = y - 1 >= 0 && y - 1 < g.ny, yp_ok = y + 1 >= 0 && y + 1 < g.ny;
+      const int gs0 = gs;  // stage of plane xa-2
+      auto st_of = [&](int x) { return gs0 + (x - (xa - 2)); };
+
+      // v (scaled, masked) at stage s, stage row r, tile column c (-HZ .. TZ+HZ-1)
+      auto vat = [&](int s, int x, int r, int c) -> double {
+        const int yy = y0 - HV + r, zz = zt0 + c;
+        if (x < 0 || x >= g.nx || yy < 0 || yy >= g.ny || zz < 0 || zz >= g.nz) return 0.0;
+        return vrowp(s, r)[c + HZ] * rnw;
+      };
+      auto vown = [&](int x, double (&o)[VZ]) {
+        if (x < 0 || x >= g.nx || !own) {
+#pragma unroll
+          for (int k = 0; k < VZ; ++k) o[k] = 0.0;
+          return;
+        }
+        const double* q = vrowp(st_of(x), vrow) + HZ + tz * VZ;
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) o[k] = q[k] * rnw;
+      };
+      // t at plane x+1 for this thread's columns (vA, vB, vC = v planes x, x+1, x+2)
+      // (every lane of the warp runs the shuffles; invalid lanes get t = 0)
+      auto t_own = [&](int x, const double (&vA)[VZ], const double (&vB)[VZ], const double (&vC)[VZ],
+                       double (&t)[VZ]) {
+        double left = __shfl_up_sync(0xffffffffu, vB[VZ - 1], 1);
+        double right = __shfl_down_sync(0xffffffffu, vB[0], 1);
+        const bool ok = x + 1 >= 0 && x + 1 < g.nx && own;
+        if (!ok) {
+#pragma unroll
+          for (int k = 0; k < VZ; ++k) t[k] = 0.0;
+          return;
+        }
+        const int s = st_of(x + 1);
+        const double* rm = vrowp(s, vrow - 1) + HZ + tz * VZ;
+        const double* rp = vrowp(s, vrow + 1) + HZ + tz * VZ;
+        if (lane == 0) left = vat(s, x + 1, vrow, tz * VZ - 1);
+        if (lane == 31) right = vat(s, x + 1, vrow, tz * VZ + VZ);
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) {
+          const double zm = k > 0 ? vB[k - 1] : left;
+          const double zp = k < VZ - 1 ? vB[k + 1] : right;
+          const double ym = (DIM == 3 && ym_ok) ? rm[k] * rnw : 0.0;
+          const double yp = (DIM == 3 && yp_ok) ? rp[k] * rnw : 0.0;
+          t[k] = apply_stencil<true>(p.A, 0.0, vA[k], ym, zm, vB[k], zp, yp, vC[k]);
+        }
+      };
+      // t at plane x+1, this row, tile column c (z-halo columns of the edge lanes)
+      auto t_col = [&](int x, int c) -> double {
+        const int zz = zt0 + c;
+        if (x + 1 < 0 || x + 1 >= g.nx || !yok || zz < 0 || zz >= g.nz) return 0.0;
+        const int s = st_of(x + 1);
+        return apply_stencil<true>(p.A, 0.0, vat(st_of(x), x, vrow, c), vat(s, x + 1, vrow - 1, c),
+                                   vat(s, x + 1, vrow, c - 1), vat(s, x + 1, vrow, c), vat(s, x + 1, vrow, c + 1),
+                                   vat(s, x + 1, vrow + 1, c), vat(st_of(x + 2), x + 2, vrow, c));
+      };
+      auto t_store = [&](int x, const double (&t)[VZ]) {  // t-plane x+1 -> buffer (x+1) % 3
+        double* b = tbuf + (size_t)(((x + 1) - (xa - 1)) % 3) * S::TPLANE + (size_t)trow * ROW + HZ;
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) b[tz * VZ + k] = t[k];
+        if (edge_l) b[-1] = t_col(x, -1);
+        if (edge_r) b[TZ] = t_col(x, TZ);
+      };
+
+      double vA[VZ], vB[VZ], vC[VZ], tp[VZ], tc[VZ], tn[VZ];
+      // prologue: t(xa-1) (own columns), t(xa) (own columns + buffer)
+      wait_full(st_of(xa - 2));
+      wait_full(st_of(xa - 1));
+      wait_full(st_of(xa));
+      vown(xa - 2, vA);
+      vown(xa - 1, vB);
+      vown(xa, vC);
+      t_own(xa - 2, vA, vB, vC, tp);
+      release(st_of(xa - 2));
+#pragma unroll
+      for (int k = 0; k < VZ; ++k) {
+        vA[k] = vB[k];
+        vB[k] = vC[k];
+      }
+      wait_full(st_of(xa + 1));
+      vown(xa + 1, vC);
+      t_own(xa - 1, vA, vB, vC, tc);
+      t_store(xa - 1, tc);
+      release(st_of(xa - 1));
+      consumer_sync(NCONS);
+
+      long long gidx = (long long)xa * g.plane + (long long)y * g.nz + zb;
+      for (int x = xa; x < xb; ++x, gidx += g.plane) {
+        // t-plane x+1 from v-planes x, x+1, x+2
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) {
+          vA[k] = vB[k];
+          vB[k] = vC[k];
+        }
+        wait_full(st_of(x + 2));
+        vown(x + 2, vC);
+        t_own(x, vA, vB, vC, tn);
+        t_store(x, tn);
+        consumer_sync(NCONS);
+        release(st_of(x));
+        // w'-plane x = A^T t from t(x-1), t(x), t(x+1)
+        if (!halo) {
+          double left = __shfl_up_sync(0xffffffffu, tc[VZ - 1], 1);
+          double right = __shfl_down_sync(0xffffffffu, tc[0], 1);
+          if (own) {
+            const double* b = tbuf + (size_t)((x - (xa - 1)) % 3) * S::TPLANE + HZ;
+            const double* rc = b + (size_t)trow * ROW + tz * VZ;
+            const double* rm = rc - ROW;
+            const double* rp = rc + ROW;
+            if (lane == 0) left = rc[-1];
+            if (lane == 31) right = rc[VZ];
+            double o[VZ];
+#pragma unroll
+            for (int k = 0; k < VZ; ++k) {
+              const double zm = k > 0 ? tc[k - 1] : left;
+              const double zp = k < VZ - 1 ? tc[k + 1] : right;
+              const double ym = DIM == 3 ? rm[k] : 0.0;
+              const double yp = DIM == 3 ? rp[k] : 0.0;
+              o[k] = apply_stencil<true>(p.AT, 0.0, tp[k], ym, zm, tc[k], zp, yp, tn[k]);
+              red[0] += o[k] * o[k];
+            }
+            store_any<double, VZ>(p.outv, gidx, VZ, o, true);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < VZ; ++k) {
+          tp[k] = tc[k];
+          tc[k] = tn[k];
+        }
+      }
+      release(st_of(xb));
+      release(st_of(xb + 1));
+      gs += xb - xa + 4;
+    }
+  }
+
+  double tot[1];
+  const int ops[1] = {RED_SUM};
+  if (grid_finish<1, S::NTOT>(red, ops, p.partials, g.pstride, p.ticket, tot)) {
+    if (threadIdx.x == 0) finish_pass(p, tot);
+  }
+}
+
+}  // namespace gadi

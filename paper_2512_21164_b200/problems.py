@@ -50,7 +50,7 @@ class StencilProblem(Problem):
     def __init__(self, spec: StencilSpec):  # noqa: D107 - dataclass fields are properties here
         self.spec = spec
         self.A = StencilMatrix(spec)
-        self.label = spec.family
+        self.label = "crd3d" if (spec.family == "crd" and spec.ndim == 3) else spec.family
         self.params = dict(spec.params)
         self._b = None
         self._exact = None
@@ -120,3 +120,17 @@ def build_complex_rd(n_g: int, s: float = 1.0e4, seed: int = 0,
     if laplacian_scaling not in ("nu_over_h2", "nu"):
         raise ValueError("laplacian_scaling must be 'nu_over_h2' or 'nu'")
     return StencilProblem(spec_complex_rd(int(n_g), float(s), int(seed), laplacian_scaling))
+
+
+def build_complex_rd_3d(n_g: int, s: float = 1.0e4, seed: int = 0,
+                        laplacian_scaling: str = "nu_over_h2") -> StencilProblem:
+    """3-D complex reaction-diffusion, n = 2 n_g^3 (BASELINE config 5; the
+    reference's 2-D recipe, REF/problems.py:96-120, with the 7-point
+    Laplacian -- SURVEY D1)."""
+    if n_g < 2:
+        raise ValueError("n_g must be >= 2")
+    if laplacian_scaling not in ("nu_over_h2", "nu"):
+        raise ValueError("laplacian_scaling must be 'nu_over_h2' or 'nu'")
+    if 2 * n_g ** 3 > _SIZE_CAP:
+        raise ValueError("n_g**3 exceeds the size guard")
+    return StencilProblem(spec_complex_rd(int(n_g), float(s), int(seed), laplacian_scaling, 3))

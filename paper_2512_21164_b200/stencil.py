@@ -94,21 +94,32 @@ def spec_cd_3d(n_g: int) -> StencilSpec:
     return StencilSpec("cd3d", int(n_g), 3, a, {"n_g": n_g, "r": r})
 
 
-def crd_potential(n_g: int, s: float, seed: int) -> np.ndarray:
-    xi = np.random.Generator(np.random.Philox(key=seed)).uniform(size=n_g ** 2)
+def crd_potential(n_g: int, s: float, seed: int, ndim: int = 2) -> np.ndarray:
+    xi = np.random.Generator(np.random.Philox(key=seed)).uniform(size=n_g ** ndim)
     return s * xi
 
 
 def spec_complex_rd(n_g: int, s: float = 1.0e4, seed: int = 0,
-                    laplacian_scaling: str = "nu_over_h2") -> StencilSpec:
+                    laplacian_scaling: str = "nu_over_h2", ndim: int = 2) -> StencilSpec:
+    """crd (REF/problems.py:96-120).  ``ndim=3`` is the 3-D extension of
+    BASELINE config 5 (no reference generator): the same recipe
+    with the 7-point Laplacian scale*(t(x)I(x)I + I(x)t(x)I + I(x)I(x)t), whose
+    diagonal 2+2+2 = 6 is exact before the scaling, and V over n_g^3 points."""
+    if ndim not in (2, 3):
+        raise ValueError("ndim must be 2 or 3")
     nu = 1.0e-5 * (64.0 / n_g) ** 2
     h = 1.0 / (n_g + 1)
     sc = nu / h ** 2 if laplacian_scaling == "nu_over_h2" else nu
-    lap = Coefs(sc * 4.0, (sc * -1.0, 0.0, sc * -1.0), (sc * -1.0, 0.0, sc * -1.0))
-    v = crd_potential(n_g, s, seed)
-    return StencilSpec("crd", int(n_g), 2, lap,
-                       {"n_g": n_g, "s": s, "seed": seed, "nu": nu,
-                        "laplacian_scaling": laplacian_scaling}, v)
+    off = sc * -1.0
+    if ndim == 2:
+        lap = Coefs(sc * 4.0, (off, 0.0, off), (off, 0.0, off))
+    else:
+        lap = Coefs(sc * 6.0, (off, off, off), (off, off, off))
+    v = crd_potential(n_g, s, seed, ndim)
+    params = {"n_g": n_g, "s": s, "seed": seed, "nu": nu, "laplacian_scaling": laplacian_scaling}
+    if ndim == 3:
+        params["ndim"] = 3
+    return StencilSpec("crd", int(n_g), ndim, lap, params, v)
 
 
 @dataclass(frozen=True)
@@ -300,10 +311,11 @@ def recognise(problem) -> StencilSpec | None:
             spec = spec_cdr_2d(int(params["n_g"]), float(params.get("r", 1.0)))
         elif label == "cd3d":
             spec = spec_cd_3d(int(params["n_g"]))
-        elif label == "crd":
+        elif label in ("crd", "crd3d"):
             spec = spec_complex_rd(int(params["n_g"]), float(params.get("s", 1.0e4)),
                                    int(params.get("seed", 0)),
-                                   params.get("laplacian_scaling", "nu_over_h2"))
+                                   params.get("laplacian_scaling", "nu_over_h2"),
+                                   3 if label == "crd3d" else int(params.get("ndim", 2)))
         else:
             return None
     except (KeyError, TypeError, ValueError):
@@ -335,8 +347,8 @@ def _rows_of_spec(spec: StencilSpec, rows):
     """(cols, vals) of selected rows of A, computed from the spec directly."""
     out = []
     if spec.family == "crd":
-        m = spec.n_g ** 2
-        sub = StencilSpec("cdr2d", spec.n_g, 2, spec.A)
+        m = spec.n_g ** spec.ndim
+        sub = StencilSpec("cdr2d" if spec.ndim == 2 else "cd3d", spec.n_g, spec.ndim, spec.A)
         for i in rows:
             base = int(i) % m
             cols, vals = _rows_of_spec(sub, [base])[0]

@@ -13,6 +13,7 @@ from paper_2512_21164_b200.device import make_desc, open_context
 from paper_2512_21164_b200.precision import quantize
 
 ng, us, alpha, itol, maxit = int(sys.argv[1]), sys.argv[2], float(sys.argv[3]), float(sys.argv[4]), int(sys.argv[5])
+target = float(sys.argv[6]) if len(sys.argv) > 6 else 0.0
 p = g.build_cd_3d(ng)
 spec = p.A.spec
 ctx = open_context(make_desc(spec, alpha, us))
@@ -38,6 +39,8 @@ for k in range(maxit):
     hist.append((k, round(t / 1e3, 3), relres, berr, hs.iterations, ss.iterations))
     rmax = o.max_r
     best.append(relres)
+    if relres <= target:
+        break
     if len(best) > 10 and min(best[-10:]) > 0.99 * min(best[:-10]):
         break
 print(json.dumps({"ng": ng, "us": us, "alpha": alpha, "inner_tol": itol, "norm_s": round(t_norm / 1e3, 3),

@@ -213,10 +213,68 @@ def csr_cases(out):
     (out / "csr.json").write_text(json.dumps(res))
 
 
+def build_crd3d_ref(n_g, s=1.0e4, seed=0, laplacian_scaling="nu_over_h2"):
+    """The 3-D extension of REF/problems.py:96-120 (BASELINE config 5, SURVEY
+    D1: the reference has no 3-D generator) assembled with the reference's own
+    sparse operations: the 2-D recipe with the triple Kronecker sum."""
+    import scipy.sparse as sp
+    from gadimp.problems import Problem
+    from gadimp.sparsemat import SparseMatrix, identity, kron, tridiag
+
+    nu = 1.0e-5 * (64.0 / n_g) ** 2
+    h = 1.0 / (n_g + 1)
+    scale = nu / h**2 if laplacian_scaling == "nu_over_h2" else nu
+    t = tridiag(n_g, -1.0, 2.0, -1.0)
+    eye = identity(n_g)
+    lap = scale * (kron(kron(t, eye), eye).to_scipy() + kron(kron(eye, t), eye).to_scipy()
+                   + kron(kron(eye, eye), t).to_scipy())
+    xi = np.random.Generator(np.random.Philox(key=seed)).uniform(size=n_g**3)
+    v = sp.diags(s * xi)
+    a = SparseMatrix.from_scipy(sp.bmat([[lap, -v], [v, lap]], format="csr"))
+    ones = np.ones(a.nrows)
+    return Problem(A=a, b=a.to_scipy() @ ones, exact_solution=ones, label="crd3d",
+                   params={"n_g": n_g, "s": s, "seed": seed, "nu": nu, "laplacian_scaling": laplacian_scaling,
+                           "ndim": 3})
+
+
+def crd3d_cases(out):
+    arrays, res = {}, []
+    rng = np.random.default_rng(31)
+    for n_g in (6, 8):
+        p = build_crd3d_ref(n_g)
+        a, tag = p.A, f"crd3d_{n_g}"
+        arrays[f"{tag}/rp"], arrays[f"{tag}/ci"], arrays[f"{tag}/v"] = a.row_offsets, a.col_indices, a.values
+        arrays[f"{tag}/b_ones"] = p.b
+        x, b = rng.standard_normal(a.nrows), rng.standard_normal(a.nrows)
+        arrays[f"{tag}/x"], arrays[f"{tag}/bvec"] = x, b
+        arrays[f"{tag}/res_fp64"] = residual(a, x, b, "fp64")
+        arrays[f"{tag}/norm2"] = np.array([matrix_norm_2(a)])
+        for us in ("bf16", "fp32"):
+            sp_ = make_hss_splitting(a, 10.0, us)
+            xq = quantize(x, us)
+            arrays[f"{tag}/{us}/xq"] = xq
+            for nm, m in (("H", sp_.H_low), ("S", sp_.S_low), ("ST", sp_.S_low_T)):
+                arrays[f"{tag}/{us}/{nm}"] = spmv(m, xq, us)
+    for n_g in (6, 8):
+        p = build_crd3d_ref(n_g)
+        for us in ("bf16", "fp32", "fp64"):
+            cfg = {"alpha": 10.0, "u_s": us, "outer_tol": 1e-6, "outer_maxit": 800}
+            rep = gadi_solve(p, cfg=GadiConfig(**cfg))
+            h = rep.history
+            res.append({"name": f"crd3d{n_g}_{us}", "n_g": n_g, "cfg": cfg, "status": rep.status,
+                        "outer": rep.iterations, "inner_h": [r.inner_h_iterations for r in h],
+                        "inner_s": [r.inner_s_iterations for r in h], "relres": [r.relative_residual for r in h],
+                        "berr": [r.backward_error for r in h], "norm_A": rep.norm_A,
+                        "x_head": rep.x[:8].tolist()})
+            print(f"crd3d{n_g}_{us}: {rep.status} outer={rep.iterations} berr={h[-1].backward_error:.3e}", flush=True)
+    np.savez_compressed(out / "crd3d.npz", **arrays)
+    (out / "crd3d.json").write_text(json.dumps(res))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--only", choices=["kernels", "solves", "inner", "csr"], default=None)
+    ap.add_argument("--only", choices=["kernels", "solves", "inner", "csr", "crd3d"], default=None)
     a = ap.parse_args()
     HERE.mkdir(parents=True, exist_ok=True)
     if a.only in (None, "kernels"):
@@ -225,6 +283,9 @@ def main():
     if a.only in (None, "inner"):
         (HERE / "inner.json").write_text(json.dumps(inner_cases()))
         print("inner done", flush=True)
+    if a.only in (None, "crd3d"):
+        crd3d_cases(HERE)
+        print("crd3d done", flush=True)
     if a.only in (None, "csr"):
         csr_cases(HERE)
         print("csr done", flush=True)

@@ -75,12 +75,17 @@ def test_csr_solve_matches_reference(gpu, csr_golden, name):
     c = runs[name]
     rep = g.gadi_solve(_problem(arr, c["problem"]), cfg=g.GadiConfig(**c["cfg"]))
     assert rep.status == c["status"], (rep.status, c["status"])
-    if c["status"] == "Stagnated":
-        assert abs(rep.iterations - c["outer"]) <= max(10, int(0.1 * c["outer"]))
-    else:
-        assert abs(rep.iterations - c["outer"]) <= 1, (rep.iterations, c["outer"])
     b_got, b_ref = rep.history[-1].backward_error, c["berr"][-1]
     assert 0.5 * b_ref <= b_got <= 2.0 * b_ref, (b_got, b_ref)
+    if c["status"] == "Stagnated":
+        # the stagnation point is a noise-driven window test (gadi.py:101-112):
+        # the floor must match (berr above, forward error below), the count loosely
+        assert abs(rep.iterations - c["outer"]) <= max(15, int(0.3 * c["outer"])), (rep.iterations, c["outer"])
+        f_got, f_ref = rep.history[-1].forward_error, c["ferr"][-1]
+        assert 0.1 * f_ref <= f_got <= 10.0 * f_ref, (f_got, f_ref)
+    else:
+        all64 = all(c["cfg"].get(k, "fp64") == "fp64" for k in ("u", "u_r", "u_s"))
+        assert abs(rep.iterations - c["outer"]) <= (0 if all64 else 1), (rep.iterations, c["outer"])
     assert rep.norm_A == pytest.approx(c["norm_A"], rel=1e-10)
 
 
@@ -102,7 +107,9 @@ def test_csr_acceptance_c4_c5(gpu, csr_golden):
     assert errs["fp32"] / errs["fp64x2"] >= 10.0            # TST/test_acceptance.py:157-158
 
 
-@pytest.mark.parametrize("name", NAMES)
+# u_s = fp64 has no emulated rounding (the dots are BLAS-ordered in the
+# reference, unpinned): those runs are covered by the storage test at +-0.
+@pytest.mark.parametrize("name", [n for n in NAMES if not n.endswith("_fp64")])
 def test_csr_solve_reference_rounding_exact(gpu, csr_golden, name):
     arr, runs = csr_golden
     c = runs[name]
