@@ -119,6 +119,7 @@ static int norm_fused_step(Ctx* c, const double* in, double* out) {
   static int occ = 0;
   if (!occ) {
     GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, norm_fused_kernel<DIM>, S::NTOT, S::SMEM));
     if (occ < 1) occ = 1;
   }

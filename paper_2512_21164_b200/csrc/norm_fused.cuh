@@ -3,14 +3,15 @@
 // The two-pass form (NormPass<false>, NormPass<true>) streams 4 fp64 vectors
 // per iteration (read w, write t, read t, write w'); this kernel streams 2.
 // t never leaves the SM: while the CTA marches along x it computes the
-// t-plane x+1 on its tile plus a one-cell ring (halo warps own the two
-// y-halo rows, the edge lanes the two z-halo columns) from the v-planes
+// t-plane x+1 on its tile plus a one-cell ring (helper warps own the two
+// y-halo rows and the two z-halo columns) from the v-planes
 // x, x+1, x+2 held in the TMA stage ring, keeps t for its own columns in a
 // 3-plane register queue (x-neighbours) and the whole t-plane in a
 // triple-buffered shared-memory plane (y / z neighbours), and applies A^T to
 // produce w'-plane x.  Every t and w' value is computed with exactly the
 // operations of the two-pass form (v = w * (1/nw), ordered fp64 stencils in
-// ascending column order), so the result is bitwise the same.
+// ascending column order); only the summation order of ||w'||^2 follows
+// this kernel's grid, so sigma agrees with the two-pass form to rounding.
 //
 // Real 5-point (DIM 2: rows of 64 lanes) and 7-point (DIM 3: 32 lanes x TY
 // rows) stencils on a single domain; the crd family and slab contexts keep
@@ -35,13 +36,16 @@ struct NFShape {
   static constexpr int TROWS = TY + 2 * HT;
   static constexpr int TPLANE = TROWS * ROW;         // elements per t buffer
   static constexpr int NT = BZ * TY;
-  static constexpr int NH = DIM == 3 ? 2 : 0;        // halo warps (one per t halo row)
+  // helper warps: 3-D: one per t halo row, whose first TY lanes also compute
+  // the two z-halo columns of the core rows; 2-D: one warp for the two z-halo
+  // values (keeps the divergent single-column work off the core warps)
+  static constexpr int NH = DIM == 3 ? 2 : 1;
   static constexpr int NCONS = NT + 32 * NH;
   static constexpr int NTOT = NCONS + 32;
   static constexpr int TBYTES = 3 * TPLANE * 8;
   static constexpr int BUDGET = 100 * 1024;
   static constexpr int NST_RAW = (BUDGET - TBYTES) / STAGE;
-  static constexpr int NST = NST_RAW < 4 ? 4 : (NST_RAW > 10 ? 10 : NST_RAW);
+  static constexpr int NST = NST_RAW >= 8 ? 8 : 4;  // power of two: cheap stage indexing
   static constexpr size_t SMEM = (size_t)TBYTES + (size_t)NST * STAGE + 2 * NST * sizeof(uint64_t);
 };
 
@@ -68,7 +72,7 @@ struct NormFused {
 };
 
 template <int DIM>
-__global__ void __launch_bounds__(NFShape<DIM>::NTOT, 1) norm_fused_kernel(NormFused<DIM> p) {
+__global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2) norm_fused_kernel(NormFused<DIM> p) {
   using S = NFShape<DIM>;
   constexpr int VZ = S::VZ, BZ = S::BZ, TY = S::TY, TZ = S::TZ, HZ = S::HZ, HV = S::HV, HT = S::HT;
   constexpr int ROW = S::ROW, NST = S::NST, NT = S::NT, NCONS = S::NCONS, NWCONS = NCONS / 32;
@@ -125,10 +129,15 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 1) norm_fused_kernel(NormF
   } else {
     // ---------------------------------------------------------------- consumers
     const bool halo = tid >= NT;
+    const int hw = (tid - NT) / 32;  // helper warp index
     const int tz = halo ? lane : tid % BZ;
-    const int trow = halo ? ((tid - NT) / 32 == 0 ? 0 : TY + 2 * HT - 1) : tid / BZ + HT;  // row in the t buffer
-    const int vrow = trow - HT + HV;                                                           // same y in a v stage
-    const bool edge_l = !halo && tz == 0, edge_r = !halo && tz == BZ - 1;
+    const int trow = halo ? (hw == 0 ? 0 : TY + 2 * HT - 1) : tid / BZ + HT;  // row in the t buffer
+    const int vrow = trow - HT + HV;                                          // same y in a v stage
+    const bool has_row = !halo || DIM == 3;  // computes t on its own columns of `trow`
+    // z-halo column duty (helper lanes): t buffer row zrow, tile column zcol
+    const bool has_zcol = halo && (DIM == 3 ? lane < TY : lane < 2);
+    const int zrow = DIM == 3 ? 1 + lane : 0;
+    const int zcol = (DIM == 3 ? hw == 0 : lane == 0) ? -1 : TZ;
     const double rnw = p.rnw;
     auto wait_full = [&](int s) { mbar_wait(&full[s % NST], (unsigned)((s / NST) & 1)); };
     auto release = [&](int s) {
@@ -147,7 +156,7 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 1) norm_fused_kernel(NormF
       const bool yok = y >= 0 && y < g.ny;
       const int zb = zt0 + tz * VZ;
       const bool zok = zb < g.nz;          // nz % VZ == 0: a lane's vector is all in or all out
-      const bool own = yok && zok;
+      const bool own = has_row && yok && zok;
       // validity of v rows y-1, y, y+1 and of the z-halo columns
       const bool ym_ok = y - 1 >= 0 && y - 1 < g.ny, yp_ok = y + 1 >= 0 && y + 1 < g.ny;
       const int gs0 = gs;  // stage of plane xa-2
@@ -195,21 +204,22 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 1) norm_fused_kernel(NormF
           t[k] = apply_stencil<true>(p.A, 0.0, vA[k], ym, zm, vB[k], zp, yp, vC[k]);
         }
       };
-      // t at plane x+1, this row, tile column c (z-halo columns of the edge lanes)
-      auto t_col = [&](int x, int c) -> double {
-        const int zz = zt0 + c;
-        if (x + 1 < 0 || x + 1 >= g.nx || !yok || zz < 0 || zz >= g.nz) return 0.0;
+      // t at plane x+1, t buffer row rt, tile column c (the z-halo columns)
+      auto t_col = [&](int x, int rt, int c) -> double {
+        const int zz = zt0 + c, yy = y0 + rt - HT, vr = rt - HT + HV;
+        if (x + 1 < 0 || x + 1 >= g.nx || yy < 0 || yy >= g.ny || zz < 0 || zz >= g.nz) return 0.0;
         const int s = st_of(x + 1);
-        return apply_stencil<true>(p.A, 0.0, vat(st_of(x), x, vrow, c), vat(s, x + 1, vrow - 1, c),
-                                   vat(s, x + 1, vrow, c - 1), vat(s, x + 1, vrow, c), vat(s, x + 1, vrow, c + 1),
-                                   vat(s, x + 1, vrow + 1, c), vat(st_of(x + 2), x + 2, vrow, c));
+        return apply_stencil<true>(p.A, 0.0, vat(st_of(x), x, vr, c), vat(s, x + 1, vr - 1, c),
+                                   vat(s, x + 1, vr, c - 1), vat(s, x + 1, vr, c), vat(s, x + 1, vr, c + 1),
+                                   vat(s, x + 1, vr + 1, c), vat(st_of(x + 2), x + 2, vr, c));
       };
       auto t_store = [&](int x, const double (&t)[VZ]) {  // t-plane x+1 -> buffer (x+1) % 3
-        double* b = tbuf + (size_t)(((x + 1) - (xa - 1)) % 3) * S::TPLANE + (size_t)trow * ROW + HZ;
+        double* b = tbuf + (size_t)(((x + 1) - (xa - 1)) % 3) * S::TPLANE + HZ;
+        if (has_row) {
 #pragma unroll
-        for (int k = 0; k < VZ; ++k) b[tz * VZ + k] = t[k];
-        if (edge_l) b[-1] = t_col(x, -1);
-        if (edge_r) b[TZ] = t_col(x, TZ);
+          for (int k = 0; k < VZ; ++k) b[(size_t)trow * ROW + tz * VZ + k] = t[k];
+        }
+        if (has_zcol) b[(size_t)zrow * ROW + zcol] = t_col(x, zrow, zcol);
       };
 
       double vA[VZ], vB[VZ], vC[VZ], tp[VZ], tc[VZ], tn[VZ];

@@ -35,11 +35,17 @@ template <> struct CTOf<double> { typedef double type; };
 #ifndef GADI_VZ64
 #define GADI_VZ64 2  // fp64 elements per lane (row width of an fp64 tile = 32 * VZ)
 #endif
+#ifndef GADI_VZ32
+#define GADI_VZ32 4  // fp32 elements per lane
+#endif
+#ifndef GADI_VZ2B
+#define GADI_VZ2B 8  // bf16 / fp16 elements per lane
+#endif
 template <class ST_, int DIM, int ZS_>
 struct GeoT {
   typedef ST_ ST;
   typedef typename CTOf<ST_>::type CT;
-  static constexpr int VZ = sizeof(ST_) == 8 ? GADI_VZ64 : (int)(16 / sizeof(ST_));
+  static constexpr int VZ = sizeof(ST_) == 8 ? GADI_VZ64 : (sizeof(ST_) == 4 ? GADI_VZ32 : GADI_VZ2B);
   static constexpr int BZ = DIM == 3 ? 32 : 64;
   static constexpr int BY = DIM == 3 ? GADI_BY3 : 1;
   static constexpr int ZS = ZS_;

@@ -90,7 +90,8 @@ def test_norm2_matches_reference(gpu, golden_kernels, golden_kernel_meta):
 @pytest.mark.parametrize("fam,ng", [("cdr2d", 37), ("cdr2d", 64), ("cdr2d", 100), ("cd3d", 19), ("cd3d", 20), ("cd3d", 34)])
 def test_fused_power_iteration_equals_two_pass(gpu, fam, ng, monkeypatch):
     """The one-sweep A^T A step (csrc/norm_fused.cuh) computes every t and w
-    value with the two-pass operations: identical sigma and iteration count."""
+    value with the two-pass operations; only the grid (hence the summation
+    order of ||w||^2) differs: same iteration count, sigma to rounding."""
     spec = spec_cdr_2d(ng) if fam == "cdr2d" else spec_cd_3d(ng)
     v0 = g.analysis.power_start_vector(spec.n)
     out = {}
@@ -98,4 +99,5 @@ def test_fused_power_iteration_equals_two_pass(gpu, fam, ng, monkeypatch):
         monkeypatch.setenv("GADI_NORM_2PASS", mode)
         with device.open_context(device.make_desc(spec, 1.0, "fp64")) as ctx:
             out[mode] = ctx.norm2(v0)
-    assert out["0"] == out["1"], out
+    assert out["0"][1] == out["1"][1], out
+    assert out["0"][0] == pytest.approx(out["1"][0], rel=1e-13), out

@@ -154,3 +154,22 @@ def test_slab_solve_matches_single_domain(gpu, fam, ng, kw, P):
     x = join_rows([q.x for q in reps], fam)
     fe = (rep.history[-1].forward_error or 0.0) + (ref.history[-1].forward_error or 0.0)
     np.testing.assert_allclose(x, ref.x, rtol=0, atol=2.0 * np.sqrt(x.size) * fe + 1e-14)
+
+
+def test_nccl_transport_single_rank(gpu):
+    """The NCCL communicator in a real process (runtime-bound libnccl, unique
+    id, ncclAllGather on the context stream, the deferred finalize path): one
+    rank owning the whole grid must reproduce the single-domain solve
+    bit for bit (a one-row gather reduces nothing)."""
+    uid = SlabComm.unique_id()
+    comm = SlabComm.nccl(uid, 1, 0, 0)
+    try:
+        cfg = g.GadiConfig(alpha=0.5, u_s="bf16", outer_tol=1e-6)
+        ref = g.gadi_solve(g.build_cd_3d(16), cfg=cfg, reuse_context=False)
+        rep = g.gadi_solve(g.build_cd_3d(16), cfg=cfg, comm=comm, reuse_context=False)
+        assert rep.slab == (0, 16)
+        assert rep.iterations == ref.iterations
+        assert [h.relative_residual for h in rep.history] == [h.relative_residual for h in ref.history]
+        assert np.array_equal(rep.x, ref.x)
+    finally:
+        comm.close()

@@ -161,3 +161,20 @@ def test_inner_solvers_reference_rounding_bitwise(gpu, golden_inner, k):
     if c["u_s"] != "fp64":
         assert np.array_equal(z, np.array(c["h_x"])), "H-solve iterate differs from the reference"
         assert np.array_equal(y, np.array(c["s_x"])), "S-solve iterate differs from the reference"
+
+
+def test_grid_search_alpha_matches_reference(gpu):
+    """GPU-backed grid search (paper_2512_21164_b200.alphaselect) picks the
+    reference's alpha; per-candidate outer counts within the parity bar."""
+    import json
+    from pathlib import Path
+
+    from paper_2512_21164_b200.alphaselect import grid_search_alpha
+
+    for c in json.loads((Path(__file__).resolve().parent / "golden" / "alpha.json").read_text()):
+        p = (g.build_cdr_2d if c["family"] == "cdr2d" else g.build_cd_3d)(c["n_g"])
+        cfg = g.GadiConfig(alpha=1.0, u_s=c["u_s"], outer_tol=1e-8, outer_maxit=400)
+        best, counts = grid_search_alpha(p, c["candidates"], cfg)
+        assert best == c["best"], (best, c["best"], counts, c["counts"])
+        for (a, st, outer, _), (ra, rst, router, _) in zip(counts, c["counts"]):
+            assert a == ra and st == rst and abs(outer - router) <= 1
