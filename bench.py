@@ -321,7 +321,7 @@ def run_ours(a, rank, world):
                 "berr": r64.history[-1].backward_error, "speedup_vs_fp64": round(t64 / t_solve, 3)}
 
     cpu = None
-    if rank == 0 and not a.no_cpu:
+    if rank == 0 and world == 1 and not a.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
         os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
         est, detail = cpu_sample(a, counts, "; 1 thread")
         cpu = {"value": round(est, 2), "unit": UNIT, "cores": 1, "kind": "port", "sample": detail}

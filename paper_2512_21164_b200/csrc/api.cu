@@ -101,7 +101,7 @@ static int norm_pass_d(Ctx* c, const double* in, double* out) {
 static bool norm_fused_ok(const Ctx* c) {
   if (c->kind != GADI_STENCIL || c->comm || c->no_tma) return false;
   if (getenv("GADI_NORM_2PASS") && atoi(getenv("GADI_NORM_2PASS"))) return false;
-  return ((long long)c->nz * 8) % 16 == 0 && c->nz % GADI_VZ64 == 0;
+  return ((long long)c->nz * 8) % 16 == 0 && c->nz % GADI_VZNORM == 0;
 }
 
 template <int DIM>
@@ -168,7 +168,7 @@ static void free_ctx(Ctx* c) {
       if (p) cudaFree(p);
     m = CsrDev();
   }
-  void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst, c->gbuf};
+  void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst, c->gbuf, c->wavecnt};
   for (void* p : sp)
     if (p) cudaFree(p);
   void* hp[] = {c->h_hst, c->h_sst, c->h_osum, c->h_nst};
@@ -296,6 +296,7 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   if (getenv("GADI_WAVES")) c->waves = std::max(1, atoi(getenv("GADI_WAVES")));
   if (getenv("GADI_MIN_CHUNK")) c->min_chunk = std::max(1, atoi(getenv("GADI_MIN_CHUNK")));
   if (getenv("GADI_LOCKSTEP")) c->lockstep = atoi(getenv("GADI_LOCKSTEP"));
+  if (getenv("GADI_WAVEFRONT")) c->wavefront = atoi(getenv("GADI_WAVEFRONT"));
   if (c->kind == GADI_CSR) {
     // rows as a 1-D "grid" (no stencil geometry is used)
     c->nx = (int)desc->csr_A.nrows;
@@ -390,6 +391,7 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   ALLOCG(c->RB, ns, c->ssz);
   ALLOCG(c->Y, ns, c->ssz);
   ALLOC(c->gbuf, sizeof(double) * GROW * (size_t)(c->comm ? c->comm->nranks : 1));
+  ALLOC(c->wavecnt, sizeof(unsigned) * 2 * (size_t)c->nx);
   ALLOC(c->partials, sizeof(double) * 8 * (size_t)c->pstride);
   ALLOC(c->ticket, sizeof(unsigned int));
   ALLOC(c->hst, sizeof(InnerState));
@@ -420,6 +422,7 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   CHK(cudaMallocHost((void**)&c->h_nst, sizeof(NormState)));
   for (auto& ev : c->ev) CHK(cudaEventCreate(&ev));
   CHK(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream));
+  CHK(cudaMemsetAsync(c->wavecnt, 0, sizeof(unsigned) * 2 * (size_t)c->nx, c->stream));
   CHK(cudaMemsetAsync(c->hst, 0, sizeof(InnerState), c->stream));
   CHK(cudaMemsetAsync(c->sst, 0, sizeof(InnerState), c->stream));
   if (c->kind == GADI_COMPLEX) {

@@ -100,6 +100,9 @@ struct Ctx {
   long long launches = 0;
   int no_tma = 0;  // force the register-prefetch sweep (testing)
   int waves = 1;      // grid size in waves of resident CTAs (TMA sweep)
+  int wavefront = 0;  // wavefront schedule (one CTA per tile) when the tiles fit in one wave
+  unsigned* wavecnt = nullptr;  // 2 x nx per-plane counters (alternating parity)
+  int wpar = 0;
   int min_chunk = 8;  // lower bound on planes per CTA
   int lockstep = 0;   // TMA sweep: align x-chunks across tiles (L2 halo reuse; slower on B200)
   double last_norm_ms = 0.0;

@@ -50,6 +50,8 @@ inline int launch_sweep(Ctx* c, P& p) {
   p.partials = c->partials;
   p.ticket = c->ticket;
   p.defer = defer_row(c);
+  p.wave = p.wave_clear = nullptr;
+  p.wlead = 0;
   if (tma_aligned<P>(c)) {
     // one resident wave of CTAs; the kernel splits the (tile, plane) units
     // evenly among them (SegIter)
@@ -66,6 +68,13 @@ inline int launch_sweep(Ctx* c, P& p) {
     const long long units = tiles * p.g.nx;
     const long long slots = (long long)occ * c->sms * c->waves;
     long long nbl = std::min(units, slots);
+    if (c->wavefront && c->wavecnt && tiles <= (long long)occ * c->sms && c->nx >= 4) {
+      nbl = tiles;  // one CTA per tile through all planes (SegIter with nblocks == tiles)
+      p.wave = c->wavecnt + (size_t)c->wpar * c->nx;
+      p.wave_clear = c->wavecnt + (size_t)(c->wpar ^ 1) * c->nx;
+      p.wlead = TmaShape<P>::NST + 4;
+      c->wpar ^= 1;
+    }
     if (c->lockstep && tiles <= slots) {
       // every tile split into the same k x-chunks: CTAs on neighbouring tiles
       // sweep the same planes at the same time, so y-halo rows hit in L2

@@ -21,9 +21,12 @@
 
 namespace gadi {
 
+#ifndef GADI_VZNORM
+#define GADI_VZNORM 4  // fp64 elements per lane (measured: 4 beats 2 here, not in the other fp64 passes)
+#endif
 template <int DIM>
 struct NFShape {
-  static constexpr int VZ = GADI_VZ64;
+  static constexpr int VZ = GADI_VZNORM;
   static constexpr int BZ = DIM == 3 ? 32 : 64;
   static constexpr int TY = DIM == 3 ? GADI_BY3 : 1;
   static constexpr int TZ = BZ * VZ;

@@ -50,8 +50,11 @@ struct GeoT {
   static constexpr int BY = DIM == 3 ? GADI_BY3 : 1;
   static constexpr int ZS = ZS_;
   static constexpr int NT = BZ * BY;
+// 3 CTAs per SM (register budget ~62, a 74 KB stage ring each) measured
+// 12-19% faster than 2 CTAs with a 110 KB ring on the bf16 CG/CGNR passes
+// (profiles/tiling_r01.md); the fp64 outer pass keeps 1 CTA and 110 KB.
 #ifndef GADI_TMA_MINB
-#define GADI_TMA_MINB 2
+#define GADI_TMA_MINB 3
 #endif
   static constexpr int MINB = GADI_TMA_MINB;  // CTAs per SM the TMA sweep is register-budgeted for
 };
@@ -263,6 +266,13 @@ __device__ __forceinline__ void round_vec(const CT (&a)[VZ], CT (&o)[VZ]) {
 // Common plumbing every pass carries.
 struct PassBase {
   SweepGeom g;
+  // wavefront schedule (one CTA per tile, all planes): per-plane completion
+  // counters of this launch, the other parity's counters (zeroed here for the
+  // next launch), and how many planes a producer may run ahead of the
+  // slowest CTA.  nullptr: off.
+  unsigned* wave;
+  unsigned* wave_clear;
+  int wlead;
   double* defer;  // slab decomposition: this rank's row of the gather buffer
   double* partials;
   unsigned int* ticket;

@@ -122,9 +122,12 @@ template <class P> struct TmaShape {
   static constexpr int STAGE = off_epi(P::NE);
   static constexpr int FBYTES = (int)B::SMEM;  // two f-plane buffers
 #ifndef GADI_TMA_BUDGET_KB
-#define GADI_TMA_BUDGET_KB 110
+#define GADI_TMA_BUDGET_KB 74  // smem per CTA for passes run 3 per SM
 #endif
-  static constexpr int BUDGET = GADI_TMA_BUDGET_KB * 1024;
+#ifndef GADI_TMA_BUDGET1_KB
+#define GADI_TMA_BUDGET1_KB 110  // passes budgeted for fewer CTAs per SM (MINB < 3)
+#endif
+  static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : GADI_TMA_BUDGET1_KB) * 1024;
   static constexpr int NST_RAW = (BUDGET - FBYTES) / STAGE;
   static constexpr int NST = NST_RAW < 2 ? 2 : (NST_RAW > 8 ? 8 : NST_RAW);
   static constexpr size_t SMEM = (size_t)FBYTES + (size_t)NST * STAGE + 2 * NST * sizeof(uint64_t);
@@ -200,6 +203,13 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
 #pragma unroll
   for (int s = 0; s < NR; ++s) red[s] = 0.0;
 
+  // Wavefront schedule: every CTA sweeps its tile through all nx planes and
+  // the producers may not run more than wlead planes ahead of the slowest CTA,
+  // so neighbouring tiles read the same planes at the same time and their
+  // halo rows / pad lines are served by L2 instead of DRAM.
+  if (p.wave)
+    for (int i = blockIdx.x * TH::NTOT + tid; i < g.nx; i += gridDim.x * TH::NTOT) p.wave_clear[i] = 0u;
+
   if (tid >= NCONS) {
     // ------------------------------------------------------------ producer
     // the whole warp issues the row copies of a stage (one row per lane),
@@ -227,6 +237,13 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
       for (int xp = xa - 1; xp <= xb; ++xp, ++gs) {
         const int st = gs % NST;
         if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
+        if (p.wave && xp - p.wlead >= 0) {
+          if (lane == 0) {
+            const volatile unsigned* cnt = p.wave + (xp - p.wlead);
+            while (*cnt < gridDim.x) __nanosleep(100);
+          }
+          __syncwarp();
+        }
         unsigned char* sb = stages + (size_t)st * TS::STAGE;
         const bool pv = (xp >= -g.hlo && xp < g.nx + g.hhi);
         const bool ev = pv && xp >= xa && xp < xb;
@@ -480,6 +497,10 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
           }
         consumer_sync(NCONS);
         release(s);
+        if (p.wave && tid == 0) {
+          __threadfence();
+          atomicAdd(p.wave + x, 1u);
+        }
       }
       release(gs + (xb - xa + 1));  // plane xb
       gs += xb - xa + 2;
