@@ -104,10 +104,10 @@ static bool norm_fused_ok(const Ctx* c) {
   return ((long long)c->nz * 8) % 16 == 0 && c->nz % GADI_VZNORM == 0;
 }
 
-template <int DIM>
+template <int DIM, bool DENSE>
 static int norm_fused_step(Ctx* c, const double* in, double* out) {
   using S = NFShape<DIM>;
-  NormFused<DIM> p;
+  NormFused<DIM, DENSE> p;
   p.defer = nullptr;
   p.partials = c->partials;
   p.ticket = c->ticket;
@@ -118,9 +118,10 @@ static int norm_fused_step(Ctx* c, const double* in, double* out) {
   p.AT = c->AT;
   static int occ = 0;
   if (!occ) {
-    GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-    GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, norm_fused_kernel<DIM>, S::NTOT, S::SMEM));
+    GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)S::SMEM));
+    GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM, DENSE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, norm_fused_kernel<DIM, DENSE>, S::NTOT, S::SMEM));
     if (occ < 1) occ = 1;
   }
   p.g = make_geom(c, S::TZ, S::TY, S::VZ, (long long)occ * c->sms);
@@ -128,7 +129,7 @@ static int norm_fused_step(Ctx* c, const double* in, double* out) {
   const int nb = (int)std::min<long long>(units, (long long)occ * c->sms * c->waves);
   if (nb > c->pstride) return set_error("fused norm grid exceeds partials buffer", GADI_ERR_ARG);
   prof_begin(c, K_NORM_B);
-  norm_fused_kernel<DIM><<<nb, S::NTOT, S::SMEM, c->stream>>>(p);
+  norm_fused_kernel<DIM, DENSE><<<nb, S::NTOT, S::SMEM, c->stream>>>(p);
   prof_end(c);
   c->launches++;
   GADI_CUDA(cudaGetLastError());
@@ -148,7 +149,9 @@ static cudaError_t guarded_malloc(Ctx* c, void** p, size_t bytes, size_t esz) {
   if (e != cudaSuccess) return e;
   c->raws.push_back(raw);
   *p = raw + GUARD + mb;
-  return cudaMemset(raw, 0, bytes + 2 * (GUARD + mb));
+  // on the context stream: a legacy-stream cudaMemset is not ordered with the
+  // (non-blocking) context stream and could land after the first upload
+  return cudaMemsetAsync(raw, 0, bytes + 2 * (GUARD + mb), c->stream);
 }
 // zero a vector including its halo planes
 static int zero_vec(Ctx* c, void* p, size_t esz) {
@@ -562,7 +565,12 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
     const int nb = std::min(batch, maxit - launched);
     for (int j = 0; j < nb; ++j) {
       if (fused) {
-        GADI_TRY(c->ndim == 3 ? norm_fused_step<3>(c, w, t) : norm_fused_step<2>(c, w, t));
+        // every coefficient of A nonzero (cd3d): the branch-free ordered stencil
+        const bool dense = c->A.d != 0.0 && c->A.lo[0] != 0.0 && c->A.lo[1] != 0.0 && c->A.lo[2] != 0.0 &&
+                           c->A.up[0] != 0.0 && c->A.up[1] != 0.0 && c->A.up[2] != 0.0;
+        const int rc = c->ndim == 3 ? (dense ? norm_fused_step<3, true>(c, w, t) : norm_fused_step<3, false>(c, w, t))
+                                    : norm_fused_step<2, false>(c, w, t);
+        if (rc) return rc;
         std::swap(w, t);
         continue;
       }

@@ -52,7 +52,7 @@ struct NFShape {
   static constexpr size_t SMEM = (size_t)TBYTES + (size_t)NST * STAGE + 2 * NST * sizeof(uint64_t);
 };
 
-template <int DIM>
+template <int DIM, bool DENSE>
 struct NormFused {
   SweepGeom g;
   double* defer;
@@ -74,8 +74,15 @@ struct NormFused {
   __device__ void finalize(const double (&t)[1]) const { fin_norm(ns, t[0]); }
 };
 
-template <int DIM>
-__global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2) norm_fused_kernel(NormFused<DIM> p) {
+template <int DIM, bool DENSE>
+__device__ __forceinline__ double nf_stencil(const CoefT<double>& c, double xm, double ym, double zm, double ce,
+                                             double zp, double yp, double xp) {
+  if constexpr (DENSE) return apply_stencil_dense(c, 0.0, xm, ym, zm, ce, zp, yp, xp);
+  else return apply_stencil<true>(c, 0.0, xm, ym, zm, ce, zp, yp, xp);
+}
+
+template <int DIM, bool DENSE>
+__global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2) norm_fused_kernel(NormFused<DIM, DENSE> p) {
   using S = NFShape<DIM>;
   constexpr int VZ = S::VZ, BZ = S::BZ, TY = S::TY, TZ = S::TZ, HZ = S::HZ, HV = S::HV, HT = S::HT;
   constexpr int ROW = S::ROW, NST = S::NST, NT = S::NT, NCONS = S::NCONS, NWCONS = NCONS / 32;
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2) norm_fused_kernel(NormF
           const double zp = k < VZ - 1 ? vB[k + 1] : right;
           const double ym = (DIM == 3 && ym_ok) ? rm[k] * rnw : 0.0;
           const double yp = (DIM == 3 && yp_ok) ? rp[k] * rnw : 0.0;
-          t[k] = apply_stencil<true>(p.A, 0.0, vA[k], ym, zm, vB[k], zp, yp, vC[k]);
+          t[k] = nf_stencil<DIM, DENSE>(p.A, vA[k], ym, zm, vB[k], zp, yp, vC[k]);
         }
       };
       // t at plane x+1, t buffer row rt, tile column c (the z-halo columns)
@@ -212,9 +219,9 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2) norm_fused_kernel(NormF
         const int zz = zt0 + c, yy = y0 + rt - HT, vr = rt - HT + HV;
         if (x + 1 < 0 || x + 1 >= g.nx || yy < 0 || yy >= g.ny || zz < 0 || zz >= g.nz) return 0.0;
         const int s = st_of(x + 1);
-        return apply_stencil<true>(p.A, 0.0, vat(st_of(x), x, vr, c), vat(s, x + 1, vr - 1, c),
-                                   vat(s, x + 1, vr, c - 1), vat(s, x + 1, vr, c), vat(s, x + 1, vr, c + 1),
-                                   vat(s, x + 1, vr + 1, c), vat(st_of(x + 2), x + 2, vr, c));
+        return nf_stencil<DIM, DENSE>(p.A, vat(st_of(x), x, vr, c), vat(s, x + 1, vr - 1, c),
+                                      vat(s, x + 1, vr, c - 1), vat(s, x + 1, vr, c), vat(s, x + 1, vr, c + 1),
+                                      vat(s, x + 1, vr + 1, c), vat(st_of(x + 2), x + 2, vr, c));
       };
       auto t_store = [&](int x, const double (&t)[VZ]) {  // t-plane x+1 -> buffer (x+1) % 3
         double* b = tbuf + (size_t)(((x + 1) - (xa - 1)) % 3) * S::TPLANE + HZ;
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2) norm_fused_kernel(NormF
               const double zp = k < VZ - 1 ? tc[k + 1] : right;
               const double ym = DIM == 3 ? rm[k] : 0.0;
               const double yp = DIM == 3 ? rp[k] : 0.0;
-              o[k] = apply_stencil<true>(p.AT, 0.0, tp[k], ym, zm, tc[k], zp, yp, tn[k]);
+              o[k] = nf_stencil<DIM, DENSE>(p.AT, tp[k], ym, zm, tc[k], zp, yp, tn[k]);
               red[0] += o[k] * o[k];
             }
             store_any<double, VZ>(p.outv, gidx, VZ, o, true);

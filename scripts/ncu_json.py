@@ -21,7 +21,7 @@ for k, key in names.items():
     val = lambda m: float(v[h.index(m)].replace(",", "")) * unit.get(u[h.index(m)], 1)  # noqa: E731
     rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
     t = float(v[h.index("gpu__time_duration.sum")].replace(",", ""))
-    t_us = t / 1e3 if u[h.index("gpu__time_duration.sum")] == "ns" else t
+    t_us = t * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(u[h.index("gpu__time_duration.sum")], 1.0)
     out[key] = {"kernel": v[h.index("Kernel Name")], "dram_bytes_per_launch": int(rd + wr), "dram_read": int(rd),
                 "dram_write": int(wr), "time_us_cold": t_us,
                 "dram_pct_peak": float(v[h.index("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")]),
