@@ -255,7 +255,7 @@ def run_ours(a, rank, world):
     counts = {"n": n, "outer": rep.iterations,
               "inner_h": sum(h.inner_h_iterations for h in rep.history),
               "inner_s": sum(h.inner_s_iterations for h in rep.history),
-              "norm_iters": int(prof.get("norm_b", (0, 0))[1] // max(1, a.steps)),
+              "norm_iters": rep.norm_iterations,
               "status": rep.status, "relres": rep.history[-1].relative_residual,
               "berr": rep.history[-1].backward_error, "ferr": rep.history[-1].forward_error}
     if rank == 0:
@@ -265,7 +265,16 @@ def run_ours(a, rank, world):
     # writes z, r -> 5 u_s values per unknown) and of the full H-CG iteration
     peak, peak_src = load_peaks()
     s = ssz(a.us)
-    kt = {k: (ms / cnt, cnt, ms) for k, (ms, cnt) in prof.items()}
+    # Per-kernel averages over the launches that did work: the inner loops
+    # enqueue a predicted number of iterations and the launches past
+    # convergence exit at once, so the raw launch count overstates the work;
+    # dividing each kernel's total device time (no-op launches included) by
+    # the iterations actually run gives a conservative time per real launch.
+    real = {"hcg_init": counts["outer"], "hcg_a": counts["inner_h"], "hcg_b": counts["inner_h"],
+            "cgnr_init": counts["outer"], "cgnr_p1": counts["inner_s"], "cgnr_p2": counts["inner_s"],
+            "cgnr_p3": counts["inner_s"], "outer": counts["outer"] + 1, "norm_b": counts["norm_iters"],
+            "norm_a": counts["norm_iters"]}
+    kt = {k: (ms / max(1, min(cnt, real.get(k, cnt) * a.steps)), cnt, ms) for k, (ms, cnt) in prof.items()}
     total_kernel_ms = sum(v[2] for v in kt.values())
     dom = max(kt, key=lambda k: kt[k][2])
     alg = {"hcg_a": 3 * s, "hcg_b": 5 * s, "cgnr_p1": 3 * s, "cgnr_p2": 5 * s, "cgnr_p3": 2 * s,
@@ -273,7 +282,8 @@ def run_ours(a, rank, world):
     kernels = {}
     for k, (avg_ms, cnt, tot) in kt.items():
         bpl = alg.get(k, 0) * rep_n
-        kernels[k] = {"launches": cnt, "avg_us": round(avg_ms * 1e3, 2), "share": round(tot / total_kernel_ms, 4),
+        kernels[k] = {"launches": cnt, "active_launches": min(cnt, real.get(k, cnt) * a.steps),
+                      "avg_us": round(avg_ms * 1e3, 2), "share": round(tot / total_kernel_ms, 4),
                       "alg_bytes_per_launch": bpl,
                       "achieved_gbs": round(bpl / (avg_ms * 1e-3) / 1e9, 1) if bpl else None}
     d_avg = kt[dom][0]

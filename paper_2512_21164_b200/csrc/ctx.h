@@ -101,6 +101,7 @@ struct Ctx {
   int no_tma = 0;  // force the register-prefetch sweep (testing)
   int waves = 1;      // grid size in waves of resident CTAs (TMA sweep)
   int wavefront = 0;  // wavefront schedule (one CTA per tile) when the tiles fit in one wave
+  int batch_cap = 0;  // max inner iterations enqueued per poll (0: the adaptive batch alone)
   unsigned* wavecnt = nullptr;  // 2 x nx per-plane counters (alternating parity)
   int wpar = 0;
   int min_chunk = 8;  // lower bound on planes per CTA

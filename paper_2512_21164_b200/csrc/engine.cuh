@@ -137,9 +137,12 @@ inline int poll_state(Ctx* c, InnerState* dev, InnerState* host) {
 // Enqueue inner iterations in batches (the previous solve's count + 1 first,
 // then a quarter of it), polling the device `done` flag once per batch.
 // iter(k) enqueues iteration k; passes launched after convergence are no-ops.
+// A batch cap (GADI_BATCH_CAP) bounds the no-op launches enqueued past
+// convergence when the count drops between solves, at one poll per cap.
 template <class F>
 inline int run_batched(Ctx* c, InnerState* dev, InnerState* host, int& pred, int maxit, F&& iter) {
-  int launched = 0, batch = std::max(1, pred + 1);
+  auto capped = [&](int b) { return c->batch_cap > 0 ? std::min(b, c->batch_cap) : b; };
+  int launched = 0, batch = capped(std::max(1, pred + 1));
   bool polled = false;
   while (launched < maxit) {
     const int nb = std::min(batch, maxit - launched);
@@ -148,7 +151,7 @@ inline int run_batched(Ctx* c, InnerState* dev, InnerState* host, int& pred, int
     GADI_TRY(poll_state(c, dev, host));
     polled = true;
     if (host->done) break;
-    batch = std::max(2, pred / 4 + 1);
+    batch = capped(std::max(2, pred / 4 + 1));
   }
   if (!polled) GADI_TRY(poll_state(c, dev, host));
   pred = host->it;
@@ -306,13 +309,7 @@ struct Engine {
     GADI_TRY(halo(c, c->R, sizeof(ST)));
     const CoefT<CT> H = cast_coef<CT>(c->H);
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
-    int launched = 0;
-    int batch = std::max(1, c->pred_h + 1);
-    bool polled = false;
-    while (launched < maxit) {
-      const int nb = std::min(batch, maxit - launched);
-      for (int j = 0; j < nb; ++j) {
-        const int k = launched + j;
+    GADI_TRY(run_batched(c, c->hst, c->h_hst, c->pred_h, maxit, [&](int k) {
         if (k == 0) {
           HcgA<G, true> a;
           a.st = c->hst;
@@ -338,16 +335,8 @@ struct Engine {
         b.r = (ST*)c->R;
         b.H = H;
         GADI_TRY(launch_sweep(c, b));
-        GADI_TRY(halo(c, c->R, sizeof(ST)));
-      }
-      launched += nb;
-      GADI_TRY(poll_state(c, c->hst, c->h_hst));
-      polled = true;
-      if (c->h_hst->done) break;
-      batch = std::max(2, c->pred_h / 4 + 1);
-    }
-    if (!polled) GADI_TRY(poll_state(c, c->hst, c->h_hst));
-    c->pred_h = c->h_hst->it;
+        return halo(c, c->R, sizeof(ST));
+    }));
     return halo(c, c->Z, sizeof(ST));  // z is the stencil input of the CGNR init
   }
 
@@ -369,13 +358,7 @@ struct Engine {
     GADI_TRY(launch_sweep(c, ci));
     GADI_TRY(halo(c, c->RB, sizeof(ST)));
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
-    int launched = 0;
-    int batch = std::max(1, c->pred_s + 1);
-    bool polled = false;
-    while (launched < maxit) {
-      const int nb = std::min(batch, maxit - launched);
-      for (int j = 0; j < nb; ++j) {
-        const int k = launched + j;
+    GADI_TRY(run_batched(c, c->sst, c->h_sst, c->pred_s, maxit, [&](int k) {
         if (k == 0) {
           CgnrP1<G, true> p1;
           p1.st = c->sst;
@@ -408,16 +391,8 @@ struct Engine {
         p3.rbar = (ST*)c->RB;
         p3.ST_ = STc;
         GADI_TRY(launch_sweep(c, p3));
-        GADI_TRY(halo(c, c->RB, sizeof(ST)));
-      }
-      launched += nb;
-      GADI_TRY(poll_state(c, c->sst, c->h_sst));
-      polled = true;
-      if (c->h_sst->done) break;
-      batch = std::max(2, c->pred_s / 4 + 1);
-    }
-    if (!polled) GADI_TRY(poll_state(c, c->sst, c->h_sst));
-    c->pred_s = c->h_sst->it;
+        return halo(c, c->RB, sizeof(ST));
+    }));
     return halo(c, c->Y, sizeof(ST));  // y is a field input of the outer pass
   }
 
@@ -434,12 +409,7 @@ struct Engine {
     ci.tol = tol;
     ci.maxit = maxit;
     GADI_TRY(launch_pw(c, ci));
-    int launched = 0;
-    int batch = std::max(1, c->pred_s + 1);
-    bool polled = false;
-    while (launched < maxit) {
-      const int nb = std::min(batch, maxit - launched);
-      for (int j = 0; j < nb; ++j) {
+    GADI_TRY(run_batched(c, c->sst, c->h_sst, c->pred_s, maxit, [&](int) {
         CP1<ST> p1;
         p1.vs = (const ST*)c->VS;
         p1.al = al;
@@ -454,16 +424,8 @@ struct Engine {
         p2.y = (ST*)c->Y;
         p2.r = (ST*)c->R;
         p2.st = c->sst;
-        GADI_TRY(launch_pw(c, p2));
-      }
-      launched += nb;
-      GADI_TRY(poll_state(c, c->sst, c->h_sst));
-      polled = true;
-      if (c->h_sst->done) break;
-      batch = std::max(2, c->pred_s / 4 + 1);
-    }
-    if (!polled) GADI_TRY(poll_state(c, c->sst, c->h_sst));
-    c->pred_s = c->h_sst->it;
+        return launch_pw(c, p2);
+    }));
     return halo(c, c->Y, sizeof(ST));
   }
 

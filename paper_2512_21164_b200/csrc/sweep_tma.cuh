@@ -33,7 +33,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp is parked by the
+// hardware until the phase completes (or the hint expires) instead of
+// spinning and taking issue slots from the warps that have work
+#ifndef GADI_MBAR_SUSPEND_NS
+#define GADI_MBAR_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+#if GADI_MBAR_SUSPEND_NS > 0
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "n"(GADI_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -43,6 +60,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
   asm volatile(

@@ -20,6 +20,13 @@ rep = g.gadi_solve(build(ng), cfg=cfg, return_x=False)
 prof = ctx.prof_read()
 ctx.prof_enable(False)
 knobs = {k: v for k, v in os.environ.items() if k.startswith("GADI_")}
+ih = sum(h.inner_h_iterations for h in rep.history)
+is_ = sum(h.inner_s_iterations for h in rep.history)
+real = {"hcg_a": ih, "hcg_b": ih, "cgnr_p1": is_, "cgnr_p2": is_, "cgnr_p3": is_, "norm_b": rep.norm_iterations,
+        "norm_a": rep.norm_iterations, "outer": rep.iterations + 1, "hcg_init": rep.iterations,
+        "cgnr_init": rep.iterations}
+# per launch that did work (no-op launches past convergence included in the time)
 print(json.dumps({"knobs": knobs, "ng": ng, "us": us,
-                  "kernels": {k: round(ms / n * 1e3, 2) for k, (ms, n) in prof.items()},
-                  "launches": {k: n for k, (ms, n) in prof.items()}}))
+                  "kernels": {k: round(ms / max(1, min(n, real.get(k, n))) * 1e3, 2) for k, (ms, n) in prof.items()},
+                  "launches": {k: n for k, (ms, n) in prof.items()}, "real": real,
+                  "total_ms": {k: round(ms, 2) for k, (ms, n) in prof.items()}}))
