@@ -301,6 +301,7 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   if (getenv("GADI_LOCKSTEP")) c->lockstep = atoi(getenv("GADI_LOCKSTEP"));
   if (getenv("GADI_WAVEFRONT")) c->wavefront = atoi(getenv("GADI_WAVEFRONT"));
   if (getenv("GADI_BATCH_CAP")) c->batch_cap = std::max(0, atoi(getenv("GADI_BATCH_CAP")));
+  if (getenv("GADI_TMA2")) c->tma2 = atoi(getenv("GADI_TMA2"));
   if (c->kind == GADI_CSR) {
     // rows as a 1-D "grid" (no stencil geometry is used)
     c->nx = (int)desc->csr_A.nrows;

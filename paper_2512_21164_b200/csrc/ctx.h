@@ -102,6 +102,7 @@ struct Ctx {
   int waves = 1;      // grid size in waves of resident CTAs (TMA sweep)
   int wavefront = 0;  // wavefront schedule (one CTA per tile) when the tiles fit in one wave
   int batch_cap = 0;  // max inner iterations enqueued per poll (0: the adaptive batch alone)
+  int tma2 = 1;       // barrier-free TMA consumers (sweep_tma2.cuh); 0: f-plane form
   unsigned* wavecnt = nullptr;  // 2 x nx per-plane counters (alternating parity)
   int wpar = 0;
   int min_chunk = 8;  // lower bound on planes per CTA

@@ -16,6 +16,11 @@
 
 namespace gadi {
 
+// Passes may opt out of the barrier-free consumer form (static TMA2_OK =
+// false): the fp64 outer pass measured faster with the f-plane form.
+template <class P, class = void> struct TmaForm2 : std::true_type {};
+template <class P> struct TmaForm2<P, std::void_t<decltype(P::TMA2_OK)>> : std::bool_constant<P::TMA2_OK> {};
+
 // True when every input row of pass P starts 16-byte aligned (TMA path).
 template <class P>
 inline bool tma_aligned(const Ctx* c) {
@@ -54,13 +59,21 @@ inline int launch_sweep(Ctx* c, P& p) {
   p.wlead = 0;
   if (tma_aligned<P>(c)) {
     // one resident wave of CTAs; the kernel splits the (tile, plane) units
-    // evenly among them (SegIter)
-    const size_t smem = TmaShape<P>::SMEM;
-    constexpr int NTH = TmaThreads<P>::NTOT;
-    static int occ = 0;
+    // evenly among them (SegIter).  Barrier-free consumers (sweep_tma2.cuh)
+    // unless GADI_TMA2=0 selects the f-plane form (sweep_tma.cuh).
+    const bool v2 = c->tma2 != 0 && TmaForm2<P>::value;
+    const size_t smem = v2 ? TmaShape2<P>::SMEM : TmaShape<P>::SMEM;
+    const int NTH = v2 ? P::NT + 32 : TmaThreads<P>::NTOT;
+    static int occ1 = 0, occ2 = 0;
+    int& occ = v2 ? occ2 : occ1;
     if (!occ) {
-      GADI_CUDA(cudaFuncSetAttribute(sweep_tma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma_kernel<P>, NTH, smem));
+      if (v2) {
+        GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P>, NTH, smem));
+      } else {
+        GADI_CUDA(cudaFuncSetAttribute(sweep_tma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma_kernel<P>, NTH, smem));
+      }
       if (occ < 1) occ = 1;
     }
     p.g = make_geom(c, S::TZ, S::TY, P::VZ, (long long)occ * c->sms);
@@ -72,7 +85,7 @@ inline int launch_sweep(Ctx* c, P& p) {
       nbl = tiles;  // one CTA per tile through all planes (SegIter with nblocks == tiles)
       p.wave = c->wavecnt + (size_t)c->wpar * c->nx;
       p.wave_clear = c->wavecnt + (size_t)(c->wpar ^ 1) * c->nx;
-      p.wlead = TmaShape<P>::NST + 4;
+      p.wlead = (v2 ? TmaShape2<P>::NST : TmaShape<P>::NST) + 4;
       c->wpar ^= 1;
     }
     if (c->lockstep && tiles <= slots) {
@@ -84,7 +97,10 @@ inline int launch_sweep(Ctx* c, P& p) {
     const int nb = (int)nbl;
     if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
     prof_begin(c, P::KID);
-    sweep_tma_kernel<P><<<nb, NTH, smem, c->stream>>>(p);
+    if (v2)
+      sweep_tma2_kernel<P><<<nb, NTH, smem, c->stream>>>(p);
+    else
+      sweep_tma_kernel<P><<<nb, NTH, smem, c->stream>>>(p);
     prof_end(c);
   } else {
     p.g = make_geom(c, S::TZ, S::TY, P::VZ);

@@ -19,7 +19,7 @@
 // and accumulate them in fp64.  u_s = fp64 runs the same code in fp64 with
 // the reference's ordered (non-FMA) stencil arithmetic.
 #pragma once
-#include "sweep_tma.cuh"
+#include "sweep_tma2.cuh"
 
 namespace gadi {
 
@@ -676,6 +676,7 @@ struct Outer : G, PassBase {
   static constexpr int NR = 6;
   static constexpr int MINB = 1;  // two fp64 fields: let ptxas keep them in registers
   static constexpr bool HAS_RED = true, ORD = true, TMA_OK = !CPLX;
+  static constexpr bool TMA2_OK = false;  // the f-plane consumer form is faster here (profiles/tiling_r01.md)
   static constexpr int KID = K_OUTER;
   static __device__ __forceinline__ int op(int s) { return s == 1 ? RED_MAX : RED_SUM; }
   const double* x;

@@ -185,6 +185,93 @@ struct SegIter {
   }
 };
 
+// The producer warp: streams every plane of this CTA's segments into the
+// stage ring (one bulk copy per row and input, issued one row per lane; lane
+// 0 posts the byte count first).  Shared by both consumer designs.
+template <class P, class TS>
+__device__ __forceinline__ void produce_stages(const P& p, const SweepGeom& g, unsigned char* stages, uint64_t* full,
+                                               uint64_t* empty, int lane) {
+  constexpr int TZ = TS::TZ, TY = TS::TY, NIN = P::NIN, NE = P::NE, NST = TS::NST;
+  constexpr int NCOPY = NIN * (TY + 2) + NE * TY;
+  SegIter it(g, gridDim.x, blockIdx.x);
+  int tile, xa, xb;
+  int gs = 0;
+  while (it.next(tile, xa, xb)) {
+    const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+    // Row spans clipped to the grid row [0, nz): the 16-byte pads and the
+    // part of a last partial tile past nz are never read by the consumers,
+    // and at a row boundary they would pull extra DRAM lines.  zt0, nz and
+    // the pads are 16-byte multiples on this path, so clipped copies stay
+    // aligned.  Input rows start at element zt0 - hz (smem offset 0).
+    int in_bytes[NIN > 0 ? NIN : 1];
+#pragma unroll
+    for (int j = 0; j < NIN; ++j) {
+      const int esz = P::in_esz(j), hz = TS::hz(esz);
+      in_bytes[j] = (min(zt0 + TZ + hz, g.nz) - max(zt0 - hz, 0)) * esz;
+    }
+    int epi_bytes[NE > 0 ? NE : 1];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) epi_bytes[j] = (min(zt0 + TZ, g.nz) - zt0) * P::epi_esz(j);
+    for (int xp = xa - 1; xp <= xb; ++xp, ++gs) {
+      const int st = gs % NST;
+      if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
+      if (p.wave && xp - p.wlead >= 0) {
+        if (lane == 0) {
+          const volatile unsigned* cnt = p.wave + (xp - p.wlead);
+          while (*cnt < gridDim.x) __nanosleep(100);
+        }
+        __syncwarp();
+      }
+      unsigned char* sb = stages + (size_t)st * TS::STAGE;
+      const bool pv = (xp >= -g.hlo && xp < g.nx + g.hhi);
+      const bool ev = pv && xp >= xa && xp < xb;
+      unsigned bytes = 0;
+      if (pv) {
+#pragma unroll
+        for (int j = 0; j < NIN; ++j)
+          if (p.in_active(j))
+            for (int r = 0; r < TY + 2; ++r) {
+              const int yy = y0 - 1 + r;
+              if (yy >= 0 && yy < g.ny) bytes += in_bytes[j];
+            }
+        if (ev) {
+#pragma unroll
+          for (int j = 0; j < NE; ++j)
+            for (int r = 0; r < TY; ++r)
+              if (y0 + r < g.ny) bytes += epi_bytes[j];
+        }
+      }
+      if (lane == 0) mbar_expect_tx(&full[st], bytes);
+      __syncwarp();
+      if (pv) {
+        for (int q = lane; q < NCOPY; q += 32) {
+          if (q < NIN * (TY + 2)) {
+            const int j = q / (TY + 2), r = q % (TY + 2);
+            const int yy = y0 - 1 + r;
+            if (!p.in_active(j) || yy < 0 || yy >= g.ny) continue;
+            const int esz = P::in_esz(j), hz = TS::hz(esz);
+            const int a = max(zt0 - hz, 0), b = min(zt0 + TZ + hz, g.nz);  // = in_e0 / in_bytes (j is runtime here)
+            const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
+            const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + a;
+            bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j) + (a - (zt0 - hz)) * esz, base + e0 * esz,
+                     (unsigned)((b - a) * esz), &full[st]);
+          } else if (ev) {
+            const int q2 = q - NIN * (TY + 2);
+            const int j = q2 / TY, r = q2 % TY;
+            const int yy = y0 + r;
+            if (yy >= g.ny) continue;
+            const int esz = P::epi_esz(j);
+            const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
+            const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0;
+            bulk_g2s(sb + TS::off_epi(j) + r * TS::rb_epi(j), base + e0 * esz,
+                     (unsigned)((min(zt0 + TZ, g.nz) - zt0) * esz), &full[st]);
+          }
+        }
+      }
+    }
+  }
+}
+
 template <class P>
 __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel(P p) {
   using S = SweepShape<P>;
@@ -232,84 +319,7 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
     // ------------------------------------------------------------ producer
     // the whole warp issues the row copies of a stage (one row per lane),
     // lane 0 posts the byte count first
-    constexpr int NCOPY = NIN * (TY + 2) + NE * TY;
-    SegIter it(g, gridDim.x, blockIdx.x);
-    int tile, xa, xb;
-    int gs = 0;
-    while (it.next(tile, xa, xb)) {
-      const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
-      // Row spans clipped to the grid row [0, nz): the 16-byte pads and the
-      // part of a last partial tile past nz are never read by the consumers,
-      // and at a row boundary they would pull extra DRAM lines.  zt0, nz and
-      // the pads are 16-byte multiples on this path, so clipped copies stay
-      // aligned.  Input rows start at element zt0 - hz (smem offset 0).
-      int in_bytes[NIN > 0 ? NIN : 1];
-#pragma unroll
-      for (int j = 0; j < NIN; ++j) {
-        const int esz = P::in_esz(j), hz = TS::hz(esz);
-        in_bytes[j] = (min(zt0 + TZ + hz, g.nz) - max(zt0 - hz, 0)) * esz;
-      }
-      int epi_bytes[NE > 0 ? NE : 1];
-#pragma unroll
-      for (int j = 0; j < NE; ++j) epi_bytes[j] = (min(zt0 + TZ, g.nz) - zt0) * P::epi_esz(j);
-      for (int xp = xa - 1; xp <= xb; ++xp, ++gs) {
-        const int st = gs % NST;
-        if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
-        if (p.wave && xp - p.wlead >= 0) {
-          if (lane == 0) {
-            const volatile unsigned* cnt = p.wave + (xp - p.wlead);
-            while (*cnt < gridDim.x) __nanosleep(100);
-          }
-          __syncwarp();
-        }
-        unsigned char* sb = stages + (size_t)st * TS::STAGE;
-        const bool pv = (xp >= -g.hlo && xp < g.nx + g.hhi);
-        const bool ev = pv && xp >= xa && xp < xb;
-        unsigned bytes = 0;
-        if (pv) {
-#pragma unroll
-          for (int j = 0; j < NIN; ++j)
-            if (p.in_active(j))
-              for (int r = 0; r < TY + 2; ++r) {
-                const int yy = y0 - 1 + r;
-                if (yy >= 0 && yy < g.ny) bytes += in_bytes[j];
-              }
-          if (ev) {
-#pragma unroll
-            for (int j = 0; j < NE; ++j)
-              for (int r = 0; r < TY; ++r)
-                if (y0 + r < g.ny) bytes += epi_bytes[j];
-          }
-        }
-        if (lane == 0) mbar_expect_tx(&full[st], bytes);
-        __syncwarp();
-        if (pv) {
-          for (int q = lane; q < NCOPY; q += 32) {
-            if (q < NIN * (TY + 2)) {
-              const int j = q / (TY + 2), r = q % (TY + 2);
-              const int yy = y0 - 1 + r;
-              if (!p.in_active(j) || yy < 0 || yy >= g.ny) continue;
-              const int esz = P::in_esz(j), hz = TS::hz(esz);
-              const int a = max(zt0 - hz, 0), b = min(zt0 + TZ + hz, g.nz);  // = in_e0 / in_bytes (j is runtime here)
-              const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
-              const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + a;
-              bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j) + (a - (zt0 - hz)) * esz, base + e0 * esz,
-                       (unsigned)((b - a) * esz), &full[st]);
-            } else if (ev) {
-              const int q2 = q - NIN * (TY + 2);
-              const int j = q2 / TY, r = q2 % TY;
-              const int yy = y0 + r;
-              if (yy >= g.ny) continue;
-              const int esz = P::epi_esz(j);
-              const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
-              const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + zt0;
-              bulk_g2s(sb + TS::off_epi(j) + r * TS::rb_epi(j), base + e0 * esz,
-                       (unsigned)((min(zt0 + TZ, g.nz) - zt0) * esz), &full[st]);
-            }
-          }
-        }
-      }
-    }
+    produce_stages<P, TS>(p, g, stages, full, empty, lane);
   } else {
     // ------------------------------------------------------------ consumers
     const bool halo_warp = tid >= NT;  // 3-D only: warp NT/32 -> row y0-1, NT/32+1 -> row y0+TY

@@ -1,0 +1,216 @@
+// Barrier-free consumer form of the TMA sweep (default; GADI_TMA2=0 selects
+// the f-plane form of sweep_tma.cuh).
+//
+// The f-plane form computes each plane's stencil fields once, stores them to
+// a shared-memory plane (plus two halo warps for the y-halo rows) and
+// synchronises all consumer warps at every plane.  Here a consumer reads
+// everything it needs straight from the TMA stage ring, which already holds
+// the (TY+2) haloed rows of every input: its own row's fields for x+1 (kept
+// in the 3-plane register queue), the y-neighbour rows' fields recomputed
+// from their raw inputs, the z-edge scalars from the row pads.  The stages
+// are read-only, so there is no named barrier, no halo warp and no f-plane
+// buffer: each warp only waits on the stage it needs and releases it when
+// done, and warps drift freely inside the ring.  Field recomputation costs
+// ALU (two extra field evaluations per element) that the barrier stalls of
+// the f-plane form cost in issue slots.
+#pragma once
+#include "sweep_tma.cuh"
+
+namespace gadi {
+
+template <class P>
+struct TmaShape2 : TmaShape<P> {
+  using Base = TmaShape<P>;
+  static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : GADI_TMA_BUDGET1_KB) * 1024;
+  static constexpr int NST_RAW = BUDGET / Base::STAGE;
+  static constexpr int NST = NST_RAW < 2 ? 2 : (NST_RAW > 12 ? 12 : NST_RAW);
+  static constexpr size_t SMEM = (size_t)NST * Base::STAGE + 2 * NST * sizeof(uint64_t);
+};
+
+template <class P>
+__global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
+  using S = SweepShape<P>;
+  using TS = TmaShape2<P>;
+  using CT = typename P::CT;
+  constexpr int VZ = S::VZ, BZ = S::BZ, BY = S::BY, ZS = S::ZS, NF = S::NF;
+  constexpr int TZ = S::TZ, TY = S::TY;
+  constexpr int NR = P::NR, NT = P::NT, NIN = P::NIN, NE = P::NE, NST = TS::NST;
+  constexpr int NWCONS = NT / 32;
+  static_assert(NIN <= 4 && NE <= 4, "at most four inputs of each kind");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* stages = smem_raw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)NST * TS::STAGE);
+  uint64_t* empty = full + NST;
+
+  if (!p.prepare()) return;
+  const SweepGeom g = p.g;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double red[NR];
+#pragma unroll
+  for (int s = 0; s < NR; ++s) red[s] = 0.0;
+  if (p.wave)
+    for (int i = blockIdx.x * (NT + 32) + tid; i < g.nx; i += gridDim.x * (NT + 32)) p.wave_clear[i] = 0u;
+
+  if (tid >= NT) {
+    produce_stages<P, TS>(p, g, stages, full, empty, lane);
+  } else {
+    const int tz = tid % BZ, ty = tid / BZ;
+    auto in_row = [&](int st, int r) {
+      SmRow R;
+      const unsigned char* sb = stages + (size_t)(st % NST) * TS::STAGE;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
+#pragma unroll
+      for (int j = 0; j < NIN; ++j)
+        R.p[j] = sb + TS::off_in(j) + r * TS::rb_in(j) + TS::hz(P::in_esz(j)) * P::in_esz(j);
+      return R;
+    };
+    auto epi_row = [&](int st, int r) {
+      SmRow R;
+      const unsigned char* sb = stages + (size_t)(st % NST) * TS::STAGE;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
+#pragma unroll
+      for (int j = 0; j < NE; ++j) R.p[j] = sb + TS::off_epi(j) + r * TS::rb_epi(j);
+      return R;
+    };
+    // fields of this lane's vector in stage row r; zeros unless valid (nv == VZ)
+    auto fields_at = [&](int st, int r, bool ok, CT (&f)[NF][VZ]) {
+      if (ok) {
+        typename P::Raw a;
+        p.load_raw_sm(a, in_row(st, r), tz * VZ);
+        if constexpr (HasFieldVec<P>::value) {
+          p.field_vec(a, f);
+        } else {
+#pragma unroll
+          for (int k = 0; k < VZ; ++k) {
+            CT t[NF];
+            p.field(a, k, t);
+#pragma unroll
+            for (int q = 0; q < NF; ++q) f[q][k] = t[q];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < VZ; ++k)
+#pragma unroll
+          for (int q = 0; q < NF; ++q) f[q][k] = CT(0);
+      }
+    };
+    // scalar field at element offset zo of stage row r (z-edges)
+    auto field_scalar = [&](int st, int r, int zo, bool ok, CT (&f)[NF]) {
+      if (ok) {
+        typename P::RawS a;
+        p.load_raw_s_sm(a, in_row(st, r), zo);
+        p.field_s(a, f);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NF; ++q) f[q] = CT(0);
+      }
+    };
+    auto release = [&](int s) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s % NST]);
+    };
+    auto wait_full = [&](int s) { mbar_wait(&full[s % NST], (unsigned)((s / NST) & 1)); };
+
+    SegIter it(g, gridDim.x, blockIdx.x);
+    int tile, xa, xb;
+    int gs = 0;  // stage sequence number of plane xa-1 of the current segment
+    while (it.next(tile, xa, xb)) {
+      const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+      const int zb = zt0 + tz * VZ;
+      const int y = y0 + ty;
+      const bool yok = y < g.ny;
+      const bool own = yok && zb < g.nz;  // nz % VZ == 0 on this path
+      const bool ym_ok = BY > 1 && own && y - 1 >= 0;
+      const bool yp_ok = BY > 1 && own && y + 1 < g.ny;
+      const long long rowbase = (long long)y * g.nz + zb;
+
+      CT fprev[NF][VZ], fcur[NF][VZ], fnext[NF][VZ];
+      wait_full(gs);
+      fields_at(gs, ty + 1, own && xa - 1 >= -g.hlo, fprev);
+      release(gs);
+      wait_full(gs + 1);
+      fields_at(gs + 1, ty + 1, own, fcur);
+
+      long long gidx = (long long)xa * g.plane + rowbase;
+      for (int x = xa; x < xb; ++x, gidx += g.plane) {
+        const int s = gs + (x - xa + 1);  // stage of plane x
+        wait_full(s + 1);
+        fields_at(s + 1, ty + 1, own && x + 1 < g.nx + g.hhi, fnext);
+        CT fym[NF][VZ], fyp[NF][VZ];
+        fields_at(s, ty, ym_ok, fym);
+        fields_at(s, ty + 2, yp_ok, fyp);
+        typename P::Epi E;
+        p.load_epi_sm(E, epi_row(s, ty), tz * VZ);
+        CT st[NF][VZ];
+        // z-neighbours: shuffles inside a warp, the stage row at warp edges
+        CT zl[ZS][NF], zr[ZS][NF];
+#pragma unroll
+        for (int j = 0; j < ZS; ++j) {
+          field_scalar(s, ty + 1, tz * VZ - ZS + j, lane == 0 && own && zb - ZS + j >= 0, zl[j]);
+          field_scalar(s, ty + 1, tz * VZ + VZ + j, lane == 31 && own && zb + VZ + j < g.nz, zr[j]);
+        }
+#pragma unroll
+        for (int q = 0; q < NF; ++q) {
+          CT left[ZS], right[ZS];
+#pragma unroll
+          for (int j = 0; j < ZS; ++j) {
+            const CT fromprev = __shfl_up_sync(0xffffffffu, fcur[q][VZ - ZS + j], 1);
+            const CT fromnext = __shfl_down_sync(0xffffffffu, fcur[q][j], 1);
+            left[j] = (lane == 0) ? zl[j][q] : fromprev;
+            right[j] = (lane == 31) ? zr[j][q] : fromnext;
+          }
+          if constexpr (HasStencilVec<P>::value) {
+            p.stencil_vec(q, fprev[q], fym[q], fcur[q], left, right, fyp[q], fnext[q], st[q]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < VZ; ++k) {
+              const CT zm = (k >= ZS) ? fcur[q][k - ZS] : left[k];
+              const CT zp = (k + ZS < VZ) ? fcur[q][k + ZS] : right[k + ZS - VZ];
+              const Nb<CT> nb{fprev[q][k], fym[q][k], zm, fcur[q][k], zp, fyp[q][k], fnext[q][k]};
+              st[q][k] = p.stencil(q, k, nb, fcur, E);
+            }
+          }
+        }
+        if (own) p.epilogue(gidx, VZ, fcur, st, E, red);
+#pragma unroll
+        for (int q = 0; q < NF; ++q)
+#pragma unroll
+          for (int k = 0; k < VZ; ++k) {
+            fprev[q][k] = fcur[q][k];
+            fcur[q][k] = fnext[q][k];
+          }
+        release(s);
+        if (p.wave && tid == 0) {
+          __threadfence();
+          atomicAdd(p.wave + x, 1u);
+        }
+      }
+      release(gs + (xb - xa + 1));  // plane xb
+      gs += xb - xa + 2;
+    }
+  }
+
+  if constexpr (P::HAS_RED) {
+    double tot[NR];
+    int ops[NR];
+#pragma unroll
+    for (int s = 0; s < NR; ++s) ops[s] = P::op(s);
+    if (grid_finish<NR, P::NT + 32>(red, ops, p.partials, g.pstride, p.ticket, tot)) {
+      if (threadIdx.x == 0) finish_pass(p, tot);
+    }
+  }
+}
+
+}  // namespace gadi
