@@ -178,6 +178,10 @@ static void free_ctx(Ctx* c) {
   for (void* p : hp)
     if (p) cudaFreeHost(p);
   exact_free(c);
+  if (c->gexec_h) cudaGraphExecDestroy(c->gexec_h);
+  if (c->gexec_s) cudaGraphExecDestroy(c->gexec_s);
+  if (c->graph_h) cudaGraphDestroy(c->graph_h);
+  if (c->graph_s) cudaGraphDestroy(c->graph_s);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evpool) cudaEventDestroy(e);
@@ -302,6 +306,7 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   if (getenv("GADI_WAVEFRONT")) c->wavefront = atoi(getenv("GADI_WAVEFRONT"));
   if (getenv("GADI_BATCH_CAP")) c->batch_cap = std::max(0, atoi(getenv("GADI_BATCH_CAP")));
   if (getenv("GADI_TMA2")) c->tma2 = atoi(getenv("GADI_TMA2"));
+  if (getenv("GADI_GRAPHS")) c->graphs = atoi(getenv("GADI_GRAPHS"));
   if (c->kind == GADI_CSR) {
     // rows as a 1-D "grid" (no stencil geometry is used)
     c->nx = (int)desc->csr_A.nrows;

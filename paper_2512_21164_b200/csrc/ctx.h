@@ -103,6 +103,11 @@ struct Ctx {
   int wavefront = 0;  // wavefront schedule (one CTA per tile) when the tiles fit in one wave
   int batch_cap = 0;  // max inner iterations enqueued per poll (0: the adaptive batch alone)
   int tma2 = 1;       // barrier-free TMA consumers (sweep_tma2.cuh); 0: f-plane form
+  // device-driven inner loops: CUDA graphs whose conditional WHILE node
+  // repeats two captured iterations until the solve state is done
+  int graphs = 1;
+  cudaGraph_t graph_h = nullptr, graph_s = nullptr;
+  cudaGraphExec_t gexec_h = nullptr, gexec_s = nullptr;
   unsigned* wavecnt = nullptr;  // 2 x nx per-plane counters (alternating parity)
   int wpar = 0;
   int min_chunk = 8;  // lower bound on planes per CTA

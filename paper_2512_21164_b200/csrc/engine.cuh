@@ -174,6 +174,60 @@ inline int run_batched(Ctx* c, InnerState* dev, InnerState* host, int& pred, int
   return 0;
 }
 
+// ---------------------------------------------------------------- device-driven loops
+// The inner solvers' scalars and stop tests already live on the device; a
+// CUDA graph with a conditional WHILE node removes the host from the loop:
+// its body is two captured iterations followed by a one-thread kernel that
+// sets the loop condition from the solve state.  Used on a single domain when
+// the per-launch timers are off; the host enqueues the graph once per inner
+// solve and reads the state once at the end.
+static __global__ void loop_cond_kernel(cudaGraphConditionalHandle h, const InnerState* st) {
+  cudaGraphSetConditional(h, st->done ? 0u : 1u);
+}
+
+inline bool use_graphs(const Ctx* c) { return c->graphs && !c->comm && !c->prof; }
+
+// Build (once per context) the graph whose WHILE body is `body` (which
+// enqueues the kernels of two iterations on c->stream).
+template <class F>
+inline int build_loop_graph(Ctx* c, cudaGraph_t& graph, cudaGraphExec_t& exec, const InnerState* st, F&& body) {
+  GADI_CUDA(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle h;
+  GADI_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  GADI_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+  cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+  const long long launches = c->launches;
+  GADI_CUDA(cudaStreamBeginCaptureToGraph(c->stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  int rc = body();
+  loop_cond_kernel<<<1, 1, 0, c->stream>>>(h, st);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(c->stream, &captured);
+  c->launches = launches;  // captured, not executed
+  if (rc) return rc;
+  GADI_CUDA(e);
+  GADI_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  return 0;
+}
+
+// Run the remaining iterations of an inner solve (iteration 0 already
+// enqueued) through the loop graph, then read the state.  `kernels_per_iter`
+// counts launches for the statistics.
+inline int run_loop_graph(Ctx* c, cudaGraphExec_t exec, InnerState* dev, InnerState* host, int& pred,
+                          int kernels_per_iter) {
+  GADI_CUDA(cudaGraphLaunch(exec, c->stream));
+  GADI_TRY(poll_state(c, dev, host));
+  pred = host->it;
+  const long long pairs = std::max(1, (host->it - 1 + 1) / 2);
+  c->launches += pairs * (2LL * kernels_per_iter + 1);
+  return 0;
+}
+
 template <class ST>
 struct Engine {
   typedef typename CTOf<ST>::type CT;
@@ -325,7 +379,7 @@ struct Engine {
     GADI_TRY(halo(c, c->R, sizeof(ST)));
     const CoefT<CT> H = cast_coef<CT>(c->H);
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
-    GADI_TRY(run_batched(c, c->hst, c->h_hst, c->pred_h, maxit, [&](int k) {
+    auto iter = [&](int k) -> int {
         if (k == 0) {
           HcgA<G, true> a;
           a.st = c->hst;
@@ -352,7 +406,18 @@ struct Engine {
         b.H = H;
         GADI_TRY(launch_sweep(c, b));
         return halo(c, c->R, sizeof(ST));
-    }));
+    };
+    if (use_graphs(c) && maxit > 1) {
+      GADI_TRY(iter(0));
+      if (!c->gexec_h)
+        GADI_TRY(build_loop_graph(c, c->graph_h, c->gexec_h, c->hst, [&]() -> int {
+          GADI_TRY(iter(1));
+          return iter(2);
+        }));
+      GADI_TRY(run_loop_graph(c, c->gexec_h, c->hst, c->h_hst, c->pred_h, 2));
+    } else {
+      GADI_TRY(run_batched(c, c->hst, c->h_hst, c->pred_h, maxit, iter));
+    }
     return halo(c, c->Z, sizeof(ST));  // z is the stencil input of the CGNR init
   }
 
@@ -374,7 +439,7 @@ struct Engine {
     GADI_TRY(launch_sweep(c, ci));
     GADI_TRY(halo(c, c->RB, sizeof(ST)));
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
-    GADI_TRY(run_batched(c, c->sst, c->h_sst, c->pred_s, maxit, [&](int k) {
+    auto iter = [&](int k) -> int {
         if (k == 0) {
           CgnrP1<G, true> p1;
           p1.st = c->sst;
@@ -408,7 +473,18 @@ struct Engine {
         p3.ST_ = STc;
         GADI_TRY(launch_sweep(c, p3));
         return halo(c, c->RB, sizeof(ST));
-    }));
+    };
+    if (use_graphs(c) && maxit > 1) {
+      GADI_TRY(iter(0));
+      if (!c->gexec_s)
+        GADI_TRY(build_loop_graph(c, c->graph_s, c->gexec_s, c->sst, [&]() -> int {
+          GADI_TRY(iter(1));
+          return iter(2);
+        }));
+      GADI_TRY(run_loop_graph(c, c->gexec_s, c->sst, c->h_sst, c->pred_s, 3));
+    } else {
+      GADI_TRY(run_batched(c, c->sst, c->h_sst, c->pred_s, maxit, iter));
+    }
     return halo(c, c->Y, sizeof(ST));  // y is a field input of the outer pass
   }
 
@@ -425,7 +501,7 @@ struct Engine {
     ci.tol = tol;
     ci.maxit = maxit;
     GADI_TRY(launch_pw(c, ci));
-    GADI_TRY(run_batched(c, c->sst, c->h_sst, c->pred_s, maxit, [&](int) {
+    auto iter = [&](int) -> int {
         CP1<ST> p1;
         p1.vs = (const ST*)c->VS;
         p1.al = al;
@@ -441,7 +517,18 @@ struct Engine {
         p2.r = (ST*)c->R;
         p2.st = c->sst;
         return launch_pw(c, p2);
-    }));
+    };
+    if (use_graphs(c) && maxit > 1) {
+      GADI_TRY(iter(0));
+      if (!c->gexec_s)
+        GADI_TRY(build_loop_graph(c, c->graph_s, c->gexec_s, c->sst, [&]() -> int {
+          GADI_TRY(iter(1));
+          return iter(2);
+        }));
+      GADI_TRY(run_loop_graph(c, c->gexec_s, c->sst, c->h_sst, c->pred_s, 2));
+    } else {
+      GADI_TRY(run_batched(c, c->sst, c->h_sst, c->pred_s, maxit, iter));
+    }
     return halo(c, c->Y, sizeof(ST));
   }
 

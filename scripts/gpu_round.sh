@@ -1,6 +1,7 @@
 #!/bin/bash
-# Round-end evidence: full GPU tests, smoke, bench line, launch list and
-# ncu --set full captures of the hot passes.  Usage: scripts/gpu_round.sh TAG
+# Round-end evidence: full GPU tests, smoke, bench line, launch list.
+# (ncu --set full captures: scripts/gpu_ncu.sh -- separate call, the
+# gpurun_out/ merge is capped at 64 MiB)
 tag=${1:-r02}
 export PYTHONPATH=$PWD
 mkdir -p gpurun_out
@@ -9,7 +10,3 @@ timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench_${tag}.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_${tag}.log
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 1500 \
   --csv --log-file gpurun_out/launches_${tag}.csv python scripts/prof_step.py 512 bf16 2 > gpurun_out/launch_run_${tag}.log 2>&1
-for k in HcgA HcgB norm_fused; do
-  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:$k -s 3 -c 1 \
-    -o gpurun_out/full_${tag}_$k python scripts/prof_step.py 512 bf16 1 > gpurun_out/full_${tag}_$k.log 2>&1
-done
