@@ -195,7 +195,7 @@ __device__ __forceinline__ void produce_stages(const P& p, const SweepGeom& g, u
   constexpr int NCOPY = NIN * (TY + 2) + NE * TY;
   SegIter it(g, gridDim.x, blockIdx.x);
   int tile, xa, xb;
-  int gs = 0;
+  int gs = 0, slot = 0, round = 0;
   while (it.next(tile, xa, xb)) {
     const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
     // Row spans clipped to the grid row [0, nz): the 16-byte pads and the
@@ -213,8 +213,13 @@ __device__ __forceinline__ void produce_stages(const P& p, const SweepGeom& g, u
 #pragma unroll
     for (int j = 0; j < NE; ++j) epi_bytes[j] = (min(zt0 + TZ, g.nz) - zt0) * P::epi_esz(j);
     for (int xp = xa - 1; xp <= xb; ++xp, ++gs) {
-      const int st = gs % NST;
-      if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
+      // ring position of stage gs (incremental: no division in the loop)
+      const int st = slot;
+      if (gs >= NST) mbar_wait(&empty[st], (unsigned)((round - 1) & 1));
+      if (++slot == NST) {
+        slot = 0;
+        ++round;
+      }
       if (p.wave && xp - p.wlead >= 0) {
         if (lane == 0) {
           const volatile unsigned* cnt = p.wave + (xp - p.wlead);

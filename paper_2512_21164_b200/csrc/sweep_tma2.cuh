@@ -64,9 +64,20 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
     produce_stages<P, TS>(p, g, stages, full, empty, lane);
   } else {
     const int tz = tid % BZ, ty = tid / BZ;
+    // stages are addressed by ring slot; (slot, phase) advance incrementally
+    struct Pos {
+      int slot;
+      unsigned ph;
+      __device__ void next() {
+        if (++slot == NST) {
+          slot = 0;
+          ph ^= 1u;
+        }
+      }
+    };
     auto in_row = [&](int st, int r) {
       SmRow R;
-      const unsigned char* sb = stages + (size_t)(st % NST) * TS::STAGE;
+      const unsigned char* sb = stages + (size_t)st * TS::STAGE;
 #pragma unroll
       for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
 #pragma unroll
@@ -76,7 +87,7 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
     };
     auto epi_row = [&](int st, int r) {
       SmRow R;
-      const unsigned char* sb = stages + (size_t)(st % NST) * TS::STAGE;
+      const unsigned char* sb = stages + (size_t)st * TS::STAGE;
 #pragma unroll
       for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
 #pragma unroll
@@ -117,11 +128,11 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
         for (int q = 0; q < NF; ++q) f[q] = CT(0);
       }
     };
-    auto release = [&](int s) {
+    auto release = [&](const Pos& q) {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s % NST]);
+      if (lane == 0) mbar_arrive(&empty[q.slot]);
     };
-    auto wait_full = [&](int s) { mbar_wait(&full[s % NST], (unsigned)((s / NST) & 1)); };
+    auto wait_full = [&](const Pos& q) { mbar_wait(&full[q.slot], q.ph); };
 
     SegIter it(g, gridDim.x, blockIdx.x);
     int tile, xa, xb;
@@ -137,17 +148,21 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
       const long long rowbase = (long long)y * g.nz + zb;
 
       CT fprev[NF][VZ], fcur[NF][VZ], fnext[NF][VZ];
-      wait_full(gs);
-      fields_at(gs, ty + 1, own && xa - 1 >= -g.hlo, fprev);
-      release(gs);
-      wait_full(gs + 1);
-      fields_at(gs + 1, ty + 1, own, fcur);
+      Pos ps{gs % NST, (unsigned)((gs / NST) & 1)};  // plane xa-1
+      wait_full(ps);
+      fields_at(ps.slot, ty + 1, own && xa - 1 >= -g.hlo, fprev);
+      release(ps);
+      ps.next();  // plane xa
+      wait_full(ps);
+      fields_at(ps.slot, ty + 1, own, fcur);
+      Pos pn = ps;
 
       long long gidx = (long long)xa * g.plane + rowbase;
       for (int x = xa; x < xb; ++x, gidx += g.plane) {
-        const int s = gs + (x - xa + 1);  // stage of plane x
-        wait_full(s + 1);
-        fields_at(s + 1, ty + 1, own && x + 1 < g.nx + g.hhi, fnext);
+        const int s = ps.slot;  // stage slot of plane x
+        pn.next();              // plane x+1
+        wait_full(pn);
+        fields_at(pn.slot, ty + 1, own && x + 1 < g.nx + g.hhi, fnext);
         CT fym[NF][VZ], fyp[NF][VZ];
         fields_at(s, ty, ym_ok, fym);
         fields_at(s, ty + 2, yp_ok, fyp);
@@ -191,13 +206,14 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
             fprev[q][k] = fcur[q][k];
             fcur[q][k] = fnext[q][k];
           }
-        release(s);
+        release(ps);
+        ps = pn;
         if (p.wave && tid == 0) {
           __threadfence();
           atomicAdd(p.wave + x, 1u);
         }
       }
-      release(gs + (xb - xa + 1));  // plane xb
+      release(ps);  // plane xb
       gs += xb - xa + 2;
     }
   }
