@@ -10,6 +10,7 @@ CPU; a missing library or device raises ``GpuUnavailable``.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -93,24 +94,38 @@ def open_context(desc, device: int = 0, comm=None, slab=None) -> _lib.Context:
 
 
 _CACHE: dict = {}
+_CACHE_LOCK = threading.Lock()
 
 
 def cached_context(key, make):
-    """One live context per key (reused by repeated solves of the same
-    operator, e.g. warm-up + timed runs); the previous one is released when a
-    different operator is requested to keep HBM free."""
-    ctx = _CACHE.get(key)
+    """One live context per (key, thread) (reused by repeated solves of the
+    same operator, e.g. warm-up + timed runs); a thread's previous context is
+    released when it requests a different operator, to keep HBM free.  Per
+    thread because a context is not thread-safe and slab ranks
+    may run as threads of one process (dist.SlabComm.local)."""
+    tid = threading.get_ident()
+    with _CACHE_LOCK:
+        ctx = _CACHE.get((tid, key))
+        if ctx is None:
+            stale = [k for k in _CACHE if k[0] == tid]
+            olds = [_CACHE.pop(k) for k in stale]
+        else:
+            olds = []
+    for o in olds:
+        o.close()
     if ctx is None:
-        for k in list(_CACHE):
-            _CACHE.pop(k).close()
         ctx = make()
-        _CACHE[key] = ctx
+        with _CACHE_LOCK:
+            _CACHE[(tid, key)] = ctx
     return ctx
 
 
 def clear_cache():
-    for k in list(_CACHE):
-        _CACHE.pop(k).close()
+    with _CACHE_LOCK:
+        olds = list(_CACHE.values())
+        _CACHE.clear()
+    for o in olds:
+        o.close()
 
 
 def _require_stencil(a):
