@@ -147,7 +147,8 @@ template <class P> struct TmaShape {
 #endif
   static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : GADI_TMA_BUDGET1_KB) * 1024;
   static constexpr int NST_RAW = (BUDGET - FBYTES) / STAGE;
-  static constexpr int NST = NST_RAW < 2 ? 2 : (NST_RAW > 8 ? 8 : NST_RAW);
+  // a power of two: the consumers index the ring with % and / NST
+  static constexpr int NST = NST_RAW >= 8 ? 8 : (NST_RAW >= 4 ? 4 : 2);
   static constexpr size_t SMEM = (size_t)FBYTES + (size_t)NST * STAGE + 2 * NST * sizeof(uint64_t);
 };
 
@@ -188,10 +189,10 @@ struct SegIter {
 // The producer warp: streams every plane of this CTA's segments into the
 // stage ring (one bulk copy per row and input, issued one row per lane; lane
 // 0 posts the byte count first).  Shared by both consumer designs.
-template <class P, class TS>
+template <class P, class TS, bool EPI = true>
 __device__ __forceinline__ void produce_stages(const P& p, const SweepGeom& g, unsigned char* stages, uint64_t* full,
                                                uint64_t* empty, int lane) {
-  constexpr int TZ = TS::TZ, TY = TS::TY, NIN = P::NIN, NE = P::NE, NST = TS::NST;
+  constexpr int TZ = TS::TZ, TY = TS::TY, NIN = P::NIN, NE = EPI ? P::NE : 0, NST = TS::NST;
   constexpr int NCOPY = NIN * (TY + 2) + NE * TY;
   SegIter it(g, gridDim.x, blockIdx.x);
   int tile, xa, xb;

@@ -18,6 +18,12 @@
 
 namespace gadi {
 
+// GADI_EPI_LDG: consumers load the epilogue-only inputs (no halo) with
+// 16-byte global loads one plane ahead instead of through the TMA ring
+#ifndef GADI_EPI_LDG
+#define GADI_EPI_LDG 0
+#endif
+
 template <class P>
 struct TmaShape2 : TmaShape<P> {
   using Base = TmaShape<P>;
@@ -61,7 +67,7 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
     for (int i = blockIdx.x * (NT + 32) + tid; i < g.nx; i += gridDim.x * (NT + 32)) p.wave_clear[i] = 0u;
 
   if (tid >= NT) {
-    produce_stages<P, TS>(p, g, stages, full, empty, lane);
+    produce_stages<P, TS, !GADI_EPI_LDG>(p, g, stages, full, empty, lane);
   } else {
     const int tz = tid % BZ, ty = tid / BZ;
     // stages are addressed by ring slot; (slot, phase) advance incrementally
@@ -158,6 +164,10 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
       Pos pn = ps;
 
       long long gidx = (long long)xa * g.plane + rowbase;
+#if GADI_EPI_LDG
+      typename P::Epi En;
+      if (own) p.load_epi(En, gidx, VZ);
+#endif
       for (int x = xa; x < xb; ++x, gidx += g.plane) {
         const int s = ps.slot;  // stage slot of plane x
         pn.next();              // plane x+1
@@ -167,7 +177,12 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
         fields_at(s, ty, ym_ok, fym);
         fields_at(s, ty + 2, yp_ok, fyp);
         typename P::Epi E;
+#if GADI_EPI_LDG
+        E = En;
+        if (own && x + 1 < xb) p.load_epi(En, gidx + g.plane, VZ);
+#else
         p.load_epi_sm(E, epi_row(s, ty), tz * VZ);
+#endif
         CT st[NF][VZ];
         // z-neighbours: shuffles inside a warp, the stage row at warp edges
         CT zl[ZS][NF], zr[ZS][NF];
