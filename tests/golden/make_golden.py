@@ -274,7 +274,7 @@ def crd3d_cases(out):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--only", choices=["kernels", "solves", "inner", "csr", "crd3d"], default=None)
+    ap.add_argument("--only", choices=["kernels", "solves", "inner", "csr", "crd3d", "fp16"], default=None)
     a = ap.parse_args()
     HERE.mkdir(parents=True, exist_ok=True)
     if a.only in (None, "kernels"):
@@ -283,6 +283,17 @@ def main():
     if a.only in (None, "inner"):
         (HERE / "inner.json").write_text(json.dumps(inner_cases()))
         print("inner done", flush=True)
+    if a.only in (None, "fp16"):
+        cases = [{"name": "fp16_cdr2d32", "family": "cdr2d", "n_g": 32,
+                  "cfg": {"alpha": 1.0, "u_s": "fp16", "outer_tol": 1e-10, "outer_maxit": 800}},
+                 {"name": "fp16_cd3d16", "family": "cd3d", "n_g": 16,
+                  "cfg": {"alpha": 0.5, "u_s": "fp16", "outer_tol": 1e-6, "outer_maxit": 800}},
+                 {"name": "fp16_crd16", "family": "crd", "n_g": 16,
+                  "cfg": {"alpha": 10.0, "u_s": "fp16", "outer_tol": 1e-6, "outer_maxit": 800}}]
+        res = [run_case(c) for c in cases]
+        for r in res:
+            print(f"{r['name']}: {r['status']} outer={r['outer']}", flush=True)
+        (HERE / "solves_fp16.json").write_text(json.dumps(res))
     if a.only in (None, "crd3d"):
         crd3d_cases(HERE)
         print("crd3d done", flush=True)

@@ -1,0 +1,103 @@
+"""Size-independent checks at the benchmark size (cd3d 512^3, n = 1.34e8),
+where neither the reference nor the oracle can run: properties that hold
+exactly whatever n is.
+
+* b = A 1 (device generator) and A 1 (the ordered fp64 stencil apply) are the
+  same operations: bitwise equal, and the fp64 residual at x = 1 is exactly 0;
+* the fp64 stencil is linear to rounding: A(x + y) = A x + A y within a few ulp;
+* two slabs on one device reproduce the single-domain residual bit for bit
+  (256^3, to keep three contexts in memory);
+* the bf16 inner solve reduces the true H-residual to the requested
+  tolerance's level."""
+
+import random
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2512_21164_b200 as g
+from paper_2512_21164_b200 import device
+from paper_2512_21164_b200.dist import SlabComm, slab_range, slab_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def big():
+    spec = g.build_cd_3d(512).A.spec
+    return spec
+
+
+def test_fullsize_rhs_and_zero_residual(gpu, big):
+    spec = big
+    with device.open_context(device.make_desc(spec, 1.0, "fp64")) as ctx:
+        ctx.gen_rhs_ones()
+        b = ctx.get_rhs()
+        ones = np.ones(spec.n)
+        ax = ctx.spmv(0, ones)
+        assert np.array_equal(ax, b)
+        r = ctx.residual(ones)
+        assert not np.any(r)
+    # interior rows of b vanish to rounding (relres >> berr for cd3d)
+    assert np.abs(b.reshape(512, 512, 512)[1:-1, 1:-1, 1:-1]).max() <= 1e-15
+
+
+def test_fullsize_linearity(gpu, big):
+    spec = big
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(spec.n)
+    y = rng.standard_normal(spec.n)
+    with device.open_context(device.make_desc(spec, 1.0, "fp64")) as ctx:
+        axy = ctx.spmv(0, x + y)
+        ax = ctx.spmv(0, x)
+        ay = ctx.spmv(0, y)
+    scale = 12.0 * (np.abs(x) + np.abs(y)).max()
+    assert np.abs(axy - (ax + ay)).max() <= 8 * np.finfo(float).eps * scale
+
+
+def test_two_slabs_bitwise_at_256(gpu):
+    spec = g.build_cd_3d(256).A.spec
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(spec.n)
+    b = rng.standard_normal(spec.n)
+    with device.open_context(device.make_desc(spec, 1.0, "fp64")) as ctx:
+        ctx.set_rhs(b)
+        want = ctx.residual(x)
+    key = random.randrange(1 << 30)
+    out, errs = [None, None], []
+
+    def rank(r):
+        comm = SlabComm.local(key, 2, r)
+        try:
+            x0, x1 = slab_range(256, 2, r)
+            with device.open_context(device.make_desc(spec, 1.0, "fp64"), 0, comm=comm, slab=(x0, x1)) as c:
+                c.set_rhs(slab_rows(b, spec, x0, x1))
+                out[r] = c.residual(slab_rows(x, spec, x0, x1))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+        finally:
+            comm.close()
+
+    ts = [threading.Thread(target=rank, args=(r,), daemon=True) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(300)
+    assert not errs, errs
+    assert np.array_equal(np.concatenate(out), want)
+
+
+def test_fullsize_bf16_inner_solve(gpu, big):
+    spec = big
+    sp = g.make_hss_splitting(g.build_cd_3d(512).A, 0.0125, "bf16")
+    rng = np.random.default_rng(3)
+    rhs = g.quantize(rng.uniform(-1.0, 1.0, spec.n), "bf16")
+    z, st = g.cg_spd(sp.H_low, rhs, 1e-3, None, "bf16")
+    assert st.converged and st.iterations > 10 and st.final_relative_residual <= 1e-3
+    assert np.all(np.isfinite(z))
+    # the recurrence stopped at 1e-3; the true residual of the bf16 iterate is
+    # bounded by the storage rounding of z (u = 2^-8) times ||H||_2 ||z|| / ||rhs||
+    # (||H||_2 <= 12 + alpha for this operator)
+    bound = 1e-3 + (12.0 + 0.0125) * 2.0 ** -8 * np.linalg.norm(z) / np.linalg.norm(rhs)
+    assert st.true_relative_residual <= bound, (st.true_relative_residual, bound)
