@@ -219,4 +219,5 @@ def test_fp16_solves(gpu, name):
     assert ex.iterations == c["outer"]
     assert [h.inner_h_iterations for h in ex.history] == c["inner_h"]
     assert [h.inner_s_iterations for h in ex.history] == c["inner_s"]
-    assert np.array_equal(ex.x[:8], np.array(c["x_head"]))
+    # (the non-converged fp16 runs overflow to NaN in the reference too)
+    assert np.array_equal(ex.x[:8], np.array(c["x_head"]), equal_nan=True)
