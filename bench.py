@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--alpha", type=float, default=0.0125)
     ap.add_argument("--us", default="bf16")
     ap.add_argument("--outer-tol", type=float, default=1e-12)
-    ap.add_argument("--inner-tol", type=float, default=1e-3)
+    ap.add_argument("--inner-tol", type=float, default=1e-2)
     ap.add_argument("--outer-maxit", type=int, default=2000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -124,6 +124,14 @@ struct CplxBase : PwBase {
   const ST* vs;  // u_s image of v (one per complex point)
   CT al;         // u_s image of alpha
   __device__ void loadv(long long i, int nv, CT (&vv)[VZ]) const {
+    if (nv == VZ) {
+      // VZ / 2 consecutive potentials, one vector load (i is a multiple of VZ)
+      CT t[VZ / 2];
+      load_vec<ST, VZ / 2, true>(vs, i >> 1, t);
+#pragma unroll
+      for (int k = 0; k < VZ; k += 2) vv[k] = vv[k + 1] = t[k / 2];
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < VZ; k += 2) {
       const CT t = (k < nv) ? cvt_in<CT>(vs[(i + k) >> 1]) : CT(0);
