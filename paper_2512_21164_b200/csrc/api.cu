@@ -8,6 +8,7 @@
 #include <string>
 #include "engine.cuh"
 #include "norm_fused.cuh"
+#include "hostcopy.h"
 
 namespace gadi {
 
@@ -42,14 +43,24 @@ static int launch_1d(const Ctx* c, long long n) {
   return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)c->sms * 16));
 }
 
+// large vectors cross through the pinned double-buffered stager (hostcopy.h)
+static cudaError_t h2d(Ctx* c, double* dev, const double* host, size_t bytes) {
+  if (c->stager && bytes >= 2 * stager_chunk(c->stager)) return stager_h2d(c->stager, dev, host, bytes, c->stream);
+  return cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, c->stream);
+}
+static cudaError_t d2h(Ctx* c, double* host, const double* dev, size_t bytes) {
+  if (c->stager && bytes >= 2 * stager_chunk(c->stager)) return stager_d2h(c->stager, host, dev, bytes, c->stream);
+  return cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream);
+}
+
 // host block layout -> device internal layout (crd: interleaved)
 static int upload(Ctx* c, const double* host, double* dev) {
   if (c->kind == GADI_COMPLEX) {
-    GADI_CUDA(cudaMemcpyAsync(c->tmp, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+    GADI_CUDA(h2d(c, c->tmp, host, sizeof(double) * c->n));
     interleave_kernel<<<launch_1d(c, c->n / 2), 256, 0, c->stream>>>(c->tmp, dev, c->n / 2);
     c->launches++;
   } else {
-    GADI_CUDA(cudaMemcpyAsync(dev, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+    GADI_CUDA(h2d(c, dev, host, sizeof(double) * c->n));
   }
   GADI_CUDA(cudaGetLastError());
   return 0;
@@ -59,9 +70,9 @@ static int download(Ctx* c, const double* dev, double* host) {
   if (c->kind == GADI_COMPLEX) {
     deinterleave_kernel<<<launch_1d(c, c->n / 2), 256, 0, c->stream>>>(dev, c->tmp, c->n / 2);
     c->launches++;
-    GADI_CUDA(cudaMemcpyAsync(host, c->tmp, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    GADI_CUDA(d2h(c, host, c->tmp, sizeof(double) * c->n));
   } else {
-    GADI_CUDA(cudaMemcpyAsync(host, dev, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    GADI_CUDA(d2h(c, host, dev, sizeof(double) * c->n));
   }
   GADI_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
@@ -178,6 +189,8 @@ static void free_ctx(Ctx* c) {
   for (void* p : hp)
     if (p) cudaFreeHost(p);
   exact_free(c);
+  stager_destroy(c->stager);
+  c->stager = nullptr;
   if (c->gexec_h) cudaGraphExecDestroy(c->gexec_h);
   if (c->gexec_s) cudaGraphExecDestroy(c->gexec_s);
   if (c->graph_h) cudaGraphDestroy(c->graph_h);
@@ -430,6 +443,10 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   CHK(cudaMallocHost((void**)&c->h_sst, sizeof(InnerState)));
   CHK(cudaMallocHost((void**)&c->h_osum, sizeof(OuterSums)));
   CHK(cudaMallocHost((void**)&c->h_nst, sizeof(NormState)));
+  // vectors of >= 128 MiB cross the ABI through pinned 32 MiB chunks (falls
+  // back to direct copies if the pinned allocation fails)
+  if ((size_t)c->n * sizeof(double) >= ((size_t)128 << 20) && !std::getenv("GADI_NO_STAGER"))
+    c->stager = stager_create((size_t)32 << 20, 0);
   for (auto& ev : c->ev) CHK(cudaEventCreate(&ev));
   CHK(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream));
   CHK(cudaMemsetAsync(c->wavecnt, 0, sizeof(unsigned) * 2 * (size_t)c->nx, c->stream));

@@ -73,6 +73,7 @@ struct Ctx {
   double* xs = nullptr;
   double* v64 = nullptr;  // crd potential
   double* tmp = nullptr;  // staging for host<->device permutations
+  struct HostStager* stager = nullptr;  // pinned host staging (hostcopy.h), large n only
   // u_s vectors (typed by the engine)
   void* R = nullptr;
   void* P[2] = {nullptr, nullptr};
