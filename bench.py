@@ -275,7 +275,8 @@ def run_ours(a, rank, world):
     # the iterations actually run gives a conservative time per real launch.
     real = {"hcg_init": counts["outer"], "hcg_a": counts["inner_h"], "hcg_b": counts["inner_h"],
             "cgnr_init": counts["outer"], "cgnr_p1": counts["inner_s"], "cgnr_p2": counts["inner_s"],
-            "cgnr_p3": counts["inner_s"], "outer": counts["outer"] + 1, "norm_b": counts["norm_iters"],
+            # the last iteration of every S-solve stops at P2's relres test
+            "cgnr_p3": max(1, counts["inner_s"] - counts["outer"]), "outer": counts["outer"] + 1, "norm_b": counts["norm_iters"],
             "norm_a": counts["norm_iters"]}
     kt = {k: (ms / max(1, min(cnt, real.get(k, cnt))), cnt, ms) for k, (ms, cnt) in prof.items()}
     total_kernel_ms = sum(v[2] for v in kt.values())

@@ -22,7 +22,7 @@ ctx.prof_enable(False)
 knobs = {k: v for k, v in os.environ.items() if k.startswith("GADI_")}
 ih = sum(h.inner_h_iterations for h in rep.history)
 is_ = sum(h.inner_s_iterations for h in rep.history)
-real = {"hcg_a": ih, "hcg_b": ih, "cgnr_p1": is_, "cgnr_p2": is_, "cgnr_p3": is_, "norm_b": rep.norm_iterations,
+real = {"hcg_a": ih, "hcg_b": ih, "cgnr_p1": is_, "cgnr_p2": is_, "cgnr_p3": max(1, is_ - rep.iterations), "norm_b": rep.norm_iterations,
         "norm_a": rep.norm_iterations, "outer": rep.iterations + 1, "hcg_init": rep.iterations,
         "cgnr_init": rep.iterations}
 # per launch that did work (no-op launches past convergence included in the time)
