@@ -63,7 +63,7 @@ inline int launch_sweep(Ctx* c, P& p) {
     // unless GADI_TMA2=0 selects the f-plane form (sweep_tma.cuh).
     const bool v2 = c->tma2 != 0 && TmaForm2<P>::value;
     const size_t smem = v2 ? TmaShape2<P>::SMEM : TmaShape<P>::SMEM;
-    const int NTH = v2 ? P::NT + 32 : TmaThreads<P>::NTOT;
+    const int NTH = v2 ? Tma2Threads<P>::value : TmaThreads<P>::NTOT;
     static int occ1 = 0, occ2 = 0;
     int& occ = v2 ? occ2 : occ1;
     if (!occ) {

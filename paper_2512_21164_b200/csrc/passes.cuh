@@ -295,6 +295,9 @@ struct HcgA : G, PassBase {
   CoefT<CT> H;
   CT beta;
   static constexpr bool first = FIRST;  // iteration 0: p = r, p_in is not read
+  // sweep_tma2 in-place form: the rounded p is written over the raw p row
+  static constexpr bool INPLACE = !FIRST;
+  static constexpr int FIELD_IN = 1;
   struct Raw { CT r[G::VZ], p[G::VZ]; };
   struct RawS { CT r, p; };
   struct Epi {};
@@ -488,6 +491,8 @@ struct CgnrP1 : G, PassBase {
   CoefT<CT> S;
   CT beta;
   static constexpr bool first = FIRST;
+  static constexpr bool INPLACE = !FIRST;  // see HcgA
+  static constexpr int FIELD_IN = 1;
   struct Raw { CT rb[G::VZ], p[G::VZ]; };
   struct RawS { CT rb, p; };
   struct Epi {};

@@ -24,17 +24,116 @@ namespace gadi {
 #define GADI_EPI_LDG 0
 #endif
 
+// In-place fields (GADI_INPLACE, passes declaring INPLACE): for passes whose
+// field is a rounded function of its raw inputs (HcgA, CgnrP1: p <- r + beta p,
+// rounded to u_s), each consumer warp writes its own row's field back over
+// the raw p row of the stage it has just computed it from, and one helper
+// warp does the same for the tile's two y-halo rows.  The y-neighbour fields
+// are then loaded instead of recomputed (one field evaluation per element
+// instead of three).  A third mbarrier per slot ("fields written", all
+// consumer warps + helper) orders the writes before the neighbour reads; a
+// warp writes plane x+1 before it waits for plane x, so the wait is lagged by
+// one plane and rarely stalls.
+#ifndef GADI_INPLACE
+#define GADI_INPLACE 1
+#endif
+template <class P, class = void>
+struct HasInplace : std::false_type {};
+template <class P>
+struct HasInplace<P, std::void_t<decltype(P::INPLACE)>>
+    : std::integral_constant<bool, P::INPLACE && GADI_INPLACE != 0 && P::NF == 1 && (SweepShape<P>::BY > 1)> {};
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// address of element 0 of row r of input j in stage st
+template <class P, class TS>
+__device__ __forceinline__ unsigned char* stage_in_row(unsigned char* stages, int st, int j, int r) {
+  return stages + (size_t)st * TS::STAGE + TS::off_in(j) + r * TS::rb_in(j) + TS::hz(P::in_esz(j)) * P::in_esz(j);
+}
+
+// field of one lane's VZ-vector at row r of stage st (zeros unless ok)
+template <class P, class TS>
+__device__ __forceinline__ void stage_fields(const P& p, unsigned char* stages, int st, int r, int zo, bool ok,
+                                             typename P::CT (&f)[P::NF][SweepShape<P>::VZ]) {
+  using CT = typename P::CT;
+  constexpr int VZ = SweepShape<P>::VZ;
+  if (ok) {
+    SmRow R;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
+#pragma unroll
+    for (int j = 0; j < P::NIN; ++j) R.p[j] = stage_in_row<P, TS>(stages, st, j, r);
+    typename P::Raw a;
+    p.load_raw_sm(a, R, zo);
+    p.field_vec(a, f);
+  } else {
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) f[0][k] = CT(0);
+  }
+}
+
+// the helper warp of the in-place form: fields of the tile's two y-halo rows
+// (stage rows 0 and TY+1) for every plane whose stencils the CTA computes
+template <class P, class TS>
+__device__ void inplace_halo_rows(const P& p, const SweepGeom& g, unsigned char* stages, uint64_t* full,
+                                  uint64_t* empty, uint64_t* fdone, int lane) {
+  using CT = typename P::CT;
+  using ST = typename P::ST;
+  constexpr int VZ = SweepShape<P>::VZ, TZ = SweepShape<P>::TZ, TY = SweepShape<P>::TY, NST = TS::NST;
+  SegIter it(g, gridDim.x, blockIdx.x);
+  int tile, xa, xb;
+  int gs = 0;
+  while (it.next(tile, xa, xb)) {
+    const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+    const bool zok = zt0 + lane * VZ < g.nz;
+    const bool top_ok = zok && y0 - 1 >= 0;
+    const bool bot_ok = zok && y0 + TY < g.ny;
+    int slot = gs % NST;
+    unsigned ph = (unsigned)((gs / NST) & 1);
+    for (int x = xa - 1; x <= xb; ++x) {
+      mbar_wait(&full[slot], ph);
+      if (x >= xa && x < xb) {
+        CT f[1][VZ];
+        stage_fields<P, TS>(p, stages, slot, 0, lane * VZ, top_ok, f);
+        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, 0)), lane * VZ, VZ,
+                          f[0], true);
+        stage_fields<P, TS>(p, stages, slot, TY + 1, lane * VZ, bot_ok, f);
+        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, TY + 1)),
+                          lane * VZ, VZ, f[0], true);
+        fence_proxy_async_smem();
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&fdone[slot]);
+        mbar_arrive(&empty[slot]);
+      }
+      if (++slot == NST) {
+        slot = 0;
+        ph ^= 1u;
+      }
+    }
+    gs += xb - xa + 2;
+  }
+}
+
+template <class P>
+struct Tma2Threads {
+  static constexpr int value = P::NT + 32 + (HasInplace<P>::value ? 32 : 0);
+};
+
 template <class P>
 struct TmaShape2 : TmaShape<P> {
   using Base = TmaShape<P>;
   static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : GADI_TMA_BUDGET1_KB) * 1024;
   static constexpr int NST_RAW = BUDGET / Base::STAGE;
   static constexpr int NST = NST_RAW < 2 ? 2 : (NST_RAW > 12 ? 12 : NST_RAW);
-  static constexpr size_t SMEM = (size_t)NST * Base::STAGE + 2 * NST * sizeof(uint64_t);
+  static constexpr size_t SMEM = (size_t)NST * Base::STAGE + 3 * NST * sizeof(uint64_t);
 };
 
 template <class P>
-__global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
+__global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB) sweep_tma2_kernel(P p) {
   using S = SweepShape<P>;
   using TS = TmaShape2<P>;
   using CT = typename P::CT;
@@ -42,11 +141,14 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
   constexpr int TZ = S::TZ, TY = S::TY;
   constexpr int NR = P::NR, NT = P::NT, NIN = P::NIN, NE = P::NE, NST = TS::NST;
   constexpr int NWCONS = NT / 32;
+  constexpr bool INPL = HasInplace<P>::value;
+  constexpr int NPART = NWCONS + (INPL ? 1 : 0);  // warps that release a stage
   static_assert(NIN <= 4 && NE <= 4, "at most four inputs of each kind");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* stages = smem_raw;
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)NST * TS::STAGE);
   uint64_t* empty = full + NST;
+  uint64_t* fdone = empty + NST;
 
   if (!p.prepare()) return;
   const SweepGeom g = p.g;
@@ -55,7 +157,8 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWCONS);
+      mbar_init(&empty[s], NPART);
+      mbar_init(&fdone[s], NPART);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -66,8 +169,10 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
   if (p.wave)
     for (int i = blockIdx.x * (NT + 32) + tid; i < g.nx; i += gridDim.x * (NT + 32)) p.wave_clear[i] = 0u;
 
-  if (tid >= NT) {
+  if (tid >= NT + (INPL ? 32 : 0)) {
     produce_stages<P, TS, !GADI_EPI_LDG>(p, g, stages, full, empty, lane);
+  } else if (INPL && tid >= NT) {
+    if constexpr (INPL) inplace_halo_rows<P, TS>(p, g, stages, full, empty, fdone, lane);
   } else {
     const int tz = tid % BZ, ty = tid / BZ;
     // stages are addressed by ring slot; (slot, phase) advance incrementally
@@ -139,6 +244,17 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
       if (lane == 0) mbar_arrive(&empty[q.slot]);
     };
     auto wait_full = [&](const Pos& q) { mbar_wait(&full[q.slot], q.ph); };
+    // in-place form: publish this row's field of stage st over its raw p row
+    auto put_field = [&](int st, const CT (&f)[NF][VZ]) {
+      if constexpr (INPL) {
+        using ST = typename P::ST;
+        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, st, P::FIELD_IN, ty + 1)), tz * VZ, VZ,
+                          f[0], true);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fdone[st]);
+      }
+    };
 
     SegIter it(g, gridDim.x, blockIdx.x);
     int tile, xa, xb;
@@ -157,10 +273,15 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
       Pos ps{gs % NST, (unsigned)((gs / NST) & 1)};  // plane xa-1
       wait_full(ps);
       fields_at(ps.slot, ty + 1, own && xa - 1 >= -g.hlo, fprev);
+      if constexpr (INPL) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fdone[ps.slot]);
+      }
       release(ps);
       ps.next();  // plane xa
       wait_full(ps);
       fields_at(ps.slot, ty + 1, own, fcur);
+      put_field(ps.slot, fcur);
       Pos pn = ps;
 
       long long gidx = (long long)xa * g.plane + rowbase;
@@ -173,9 +294,17 @@ __global__ void __launch_bounds__(P::NT + 32, P::MINB) sweep_tma2_kernel(P p) {
         pn.next();              // plane x+1
         wait_full(pn);
         fields_at(pn.slot, ty + 1, own && x + 1 < g.nx + g.hhi, fnext);
+        put_field(pn.slot, fnext);
         CT fym[NF][VZ], fyp[NF][VZ];
-        fields_at(s, ty, ym_ok, fym);
-        fields_at(s, ty + 2, yp_ok, fyp);
+        if constexpr (INPL) {
+          // neighbours' fields of plane x (written one plane ago)
+          mbar_wait(&fdone[s], ps.ph);
+          lds_vec<typename P::ST, VZ>(stage_in_row<P, TS>(stages, s, P::FIELD_IN, ty), tz * VZ, fym[0]);
+          lds_vec<typename P::ST, VZ>(stage_in_row<P, TS>(stages, s, P::FIELD_IN, ty + 2), tz * VZ, fyp[0]);
+        } else {
+          fields_at(s, ty, ym_ok, fym);
+          fields_at(s, ty + 2, yp_ok, fyp);
+        }
         typename P::Epi E;
 #if GADI_EPI_LDG
         E = En;
