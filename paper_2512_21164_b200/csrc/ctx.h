@@ -2,8 +2,11 @@
 // scalar states and their pinned host mirrors.  Shared by the per-precision
 // engines (engine_*.cu) and the C-ABI (api.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <array>
+#include <map>
 #include <string>
 #include <vector>
 #include "../../include/gadi_b200.h"
@@ -107,6 +110,12 @@ struct Ctx {
   // device-driven inner loops: CUDA graphs whose conditional WHILE node
   // repeats two captured iterations until the solve state is done
   int graphs = 1;
+  // TMA tensor maps of the 3-D sweeps (tmap.cuh), encoded once per
+  // (buffer, element size, box); tmap = 0 (GADI_TMAP=0) keeps row copies
+  int tmap = 1;
+  int tm_promo = 3;  // CUtensorMapL2promotion (GADI_TM_PROMO): 0 none, 1 64B, 2 128B, 3 256B
+  void* tm_encode = nullptr;
+  std::map<std::array<long long, 4>, CUtensorMap> tmcache;
   cudaGraph_t graph_h = nullptr, graph_s = nullptr;
   cudaGraphExec_t gexec_h = nullptr, gexec_s = nullptr;
   unsigned* wavecnt = nullptr;  // 2 x nx per-plane counters (alternating parity)

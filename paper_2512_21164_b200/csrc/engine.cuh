@@ -22,6 +22,66 @@ template <class P, class = void> struct TmaForm2 : std::true_type {};
 template <class P> struct TmaForm2<P, std::void_t<decltype(P::TMA2_OK)>> : std::bool_constant<P::TMA2_OK> {};
 
 // True when every input row of pass P starts 16-byte aligned (TMA path).
+// One 3-D tensor map over a vector of esz-byte elements laid out [x][y][z]
+// (planes -hlo .. nx+hhi-1 of a slab context's allocation), box {bw, bh, 1}.
+// Cached per (pointer, esz, box); false if the driver entry point or the
+// encoding is unavailable (the caller keeps the row-copy producer).
+inline bool tm_map(Ctx* c, const void* ptr, int esz, int bw, int bh, CUtensorMap* out) {
+  const std::array<long long, 4> key{(long long)(uintptr_t)ptr, esz, bw, bh};
+  auto itc = c->tmcache.find(key);
+  if (itc != c->tmcache.end()) {
+    *out = itc->second;
+    return true;
+  }
+  if (!c->tm_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      c->tmap = 0;
+      return false;
+    }
+    c->tm_encode = fn;
+  }
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  const CUtensorMapDataType dt = esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                 : esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const long long plane = (long long)c->ny * c->nz;
+  const int hlo = c->hlo, hhi = c->hhi;
+  const char* base = static_cast<const char*>(ptr) - (long long)hlo * plane * esz;
+  const cuuint64_t dims[3] = {(cuuint64_t)c->nz, (cuuint64_t)c->ny, (cuuint64_t)(c->nx + hlo + hhi)};
+  const cuuint64_t strides[2] = {(cuuint64_t)c->nz * esz, (cuuint64_t)plane * esz};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = reinterpret_cast<EncodeFn>(c->tm_encode)(
+      &m, dt, 3, const_cast<char*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)c->tm_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  c->tmcache.emplace(key, m);
+  *out = m;
+  return true;
+}
+
+template <class P>
+inline bool tm_fill(Ctx* c, const P& p, TmapSet& tm) {
+  using TS = TmaShape2<P, true>;
+  using BX = TmBox<P, TmaShape<P>>;
+  if (c->ndim != 3 || ((long long)c->ny * c->nz) % 16) return false;
+  for (int j = 0; j < P::NIN; ++j) {
+    if (!p.in_active(j)) continue;
+    if ((uintptr_t)p.in_ptr(j) % 16 || !tm_map(c, p.in_ptr(j), P::in_esz(j), BX::BW(j), TS::TY + 2, &tm.in[j]))
+      return false;
+  }
+  for (int j = 0; j < P::NE; ++j)
+    if ((uintptr_t)p.epi_ptr(j) % 16 || !tm_map(c, p.epi_ptr(j), P::epi_esz(j), TS::TZ, TS::TY, &tm.epi[j]))
+      return false;
+  return true;
+}
+
 template <class P>
 inline bool tma_aligned(const Ctx* c) {
   if (!P::TMA_OK || c->no_tma) return false;
@@ -62,14 +122,25 @@ inline int launch_sweep(Ctx* c, P& p) {
     // evenly among them (SegIter).  Barrier-free consumers (sweep_tma2.cuh)
     // unless GADI_TMA2=0 selects the f-plane form (sweep_tma.cuh).
     const bool v2 = c->tma2 != 0 && TmaForm2<P>::value;
-    const size_t smem = v2 ? TmaShape2<P>::SMEM : TmaShape<P>::SMEM;
+    // tensor-map producer for the 3-D barrier-free passes (tmap.cuh)
+    TmapSet tm;
+    tm.ok = 0;
+    if constexpr (TmaTm<P>::value) {
+      if (v2 && c->tmap) tm.ok = tm_fill<P>(c, p, tm) ? 1 : 0;
+    }
+    const size_t smem = v2 ? (tm.ok ? TmaShape2<P, true>::SMEM : TmaShape2<P>::SMEM) : TmaShape<P>::SMEM;
     const int NTH = v2 ? Tma2Threads<P>::value : TmaThreads<P>::NTOT;
-    static int occ1 = 0, occ2 = 0;
-    int& occ = v2 ? occ2 : occ1;
+    static int occ1 = 0, occ2 = 0, occ3 = 0;
+    int& occ = v2 ? (tm.ok ? occ3 : occ2) : occ1;
     if (!occ) {
-      if (v2) {
-        GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P>, NTH, smem));
+      if (v2 && tm.ok) {
+        GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P, true>, NTH, smem));
+      } else if (v2) {
+        GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P, false>, NTH, smem));
       } else {
         GADI_CUDA(cudaFuncSetAttribute(sweep_tma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma_kernel<P>, NTH, smem));
@@ -85,7 +156,7 @@ inline int launch_sweep(Ctx* c, P& p) {
       nbl = tiles;  // one CTA per tile through all planes (SegIter with nblocks == tiles)
       p.wave = c->wavecnt + (size_t)c->wpar * c->nx;
       p.wave_clear = c->wavecnt + (size_t)(c->wpar ^ 1) * c->nx;
-      p.wlead = (v2 ? TmaShape2<P>::NST : TmaShape<P>::NST) + 4;
+      p.wlead = (v2 ? (tm.ok ? TmaShape2<P, true>::NST : TmaShape2<P>::NST) : TmaShape<P>::NST) + 4;
       c->wpar ^= 1;
     }
     if (c->lockstep && tiles <= slots) {
@@ -97,8 +168,10 @@ inline int launch_sweep(Ctx* c, P& p) {
     const int nb = (int)nbl;
     if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
     prof_begin(c, P::KID);
-    if (v2)
-      sweep_tma2_kernel<P><<<nb, NTH, smem, c->stream>>>(p);
+    if (v2 && tm.ok)
+      sweep_tma2_kernel<P, true><<<nb, NTH, smem, c->stream>>>(p, tm);
+    else if (v2)
+      sweep_tma2_kernel<P, false><<<nb, NTH, smem, c->stream>>>(p, TmapNone{0});
     else
       sweep_tma_kernel<P><<<nb, NTH, smem, c->stream>>>(p);
     prof_end(c);

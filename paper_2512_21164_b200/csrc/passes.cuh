@@ -318,9 +318,9 @@ struct HcgA : G, PassBase {
   static constexpr int NIN = 2, NE = 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return 1; }
-  __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)r : (const void*)pin; }
-  __device__ const void* epi_ptr(int) const { return nullptr; }
-  __device__ bool in_active(int j) const { return j == 0 || !first; }
+  __host__ __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)r : (const void*)pin; }
+  __host__ __device__ const void* epi_ptr(int) const { return nullptr; }
+  __host__ __device__ bool in_active(int j) const { return j == 0 || !first; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const {
     lds_vec<ST, G::VZ>(R.p[0], z, a.r);
     if (!first) lds_vec<ST, G::VZ>(R.p[1], z, a.p);
@@ -382,9 +382,9 @@ struct HcgB : G, PassBase {
   static constexpr int NIN = 1, NE = 2;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return (int)sizeof(ST); }
-  __device__ const void* in_ptr(int) const { return p; }
-  __device__ const void* epi_ptr(int j) const { return j == 0 ? (const void*)z : (const void*)r; }
-  __device__ bool in_active(int) const { return true; }
+  __host__ __device__ const void* in_ptr(int) const { return p; }
+  __host__ __device__ const void* epi_ptr(int j) const { return j == 0 ? (const void*)z : (const void*)r; }
+  __host__ __device__ bool in_active(int) const { return true; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.p); }
   __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.p = lds1<ST, CT>(R.p[0], zo); }
   __device__ void load_epi_sm(Epi& e, const SmRow& R, int zo) const {
@@ -442,9 +442,9 @@ struct CgnrInit : G, PassBase {
   static constexpr int NIN = 1, NE = 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return 1; }
-  __device__ const void* in_ptr(int) const { return z; }
-  __device__ const void* epi_ptr(int) const { return nullptr; }
-  __device__ bool in_active(int) const { return true; }
+  __host__ __device__ const void* in_ptr(int) const { return z; }
+  __host__ __device__ const void* epi_ptr(int) const { return nullptr; }
+  __host__ __device__ bool in_active(int) const { return true; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.z); }
   __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.z = lds1<ST, CT>(R.p[0], zo); }
   __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
@@ -513,9 +513,9 @@ struct CgnrP1 : G, PassBase {
   static constexpr int NIN = 2, NE = 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return 1; }
-  __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)rbar : (const void*)pin; }
-  __device__ const void* epi_ptr(int) const { return nullptr; }
-  __device__ bool in_active(int j) const { return j == 0 || !first; }
+  __host__ __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)rbar : (const void*)pin; }
+  __host__ __device__ const void* epi_ptr(int) const { return nullptr; }
+  __host__ __device__ bool in_active(int j) const { return j == 0 || !first; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const {
     lds_vec<ST, G::VZ>(R.p[0], z, a.rb);
     if (!first) lds_vec<ST, G::VZ>(R.p[1], z, a.p);
@@ -577,9 +577,9 @@ struct CgnrP2 : G, PassBase {
   static constexpr int NIN = 1, NE = 2;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return (int)sizeof(ST); }
-  __device__ const void* in_ptr(int) const { return p; }
-  __device__ const void* epi_ptr(int j) const { return j == 0 ? (const void*)y : (const void*)r; }
-  __device__ bool in_active(int) const { return true; }
+  __host__ __device__ const void* in_ptr(int) const { return p; }
+  __host__ __device__ const void* epi_ptr(int j) const { return j == 0 ? (const void*)y : (const void*)r; }
+  __host__ __device__ bool in_active(int) const { return true; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.p); }
   __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.p = lds1<ST, CT>(R.p[0], zo); }
   __device__ void load_epi_sm(Epi& e, const SmRow& R, int zo) const {
@@ -633,9 +633,9 @@ struct CgnrP3 : G, PassBase {
   static constexpr int NIN = 1, NE = 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return 1; }
-  __device__ const void* in_ptr(int) const { return r; }
-  __device__ const void* epi_ptr(int) const { return nullptr; }
-  __device__ bool in_active(int) const { return true; }
+  __host__ __device__ const void* in_ptr(int) const { return r; }
+  __host__ __device__ const void* epi_ptr(int) const { return nullptr; }
+  __host__ __device__ bool in_active(int) const { return true; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.r); }
   __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.r = lds1<ST, CT>(R.p[0], zo); }
   __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
@@ -704,9 +704,9 @@ struct Outer : G, PassBase {
   static constexpr int NIN = HAS_E ? 3 : 2, NE = 1;
   static constexpr int in_esz(int j) { return j == 1 ? (int)sizeof(SU) : 8; }
   static constexpr int epi_esz(int) { return 8; }
-  __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)x : (j == 1 ? (const void*)y : (const void*)xs); }
-  __device__ const void* epi_ptr(int) const { return b; }
-  __device__ bool in_active(int j) const { return j < 2 || !ones; }
+  __host__ __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)x : (j == 1 ? (const void*)y : (const void*)xs); }
+  __host__ __device__ const void* epi_ptr(int) const { return b; }
+  __host__ __device__ bool in_active(int j) const { return j < 2 || !ones; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const {
     lds_vec<double, VZ>(R.p[0], z, a.x);
     lds_vec<SU, VZ>(R.p[1], z, a.y);
@@ -849,9 +849,9 @@ struct NormPass : G, PassBase {
   static constexpr int NIN = 1, NE = 0;
   static constexpr int in_esz(int) { return 8; }
   static constexpr int epi_esz(int) { return 1; }
-  __device__ const void* in_ptr(int) const { return in; }
-  __device__ const void* epi_ptr(int) const { return nullptr; }
-  __device__ bool in_active(int) const { return true; }
+  __host__ __device__ const void* in_ptr(int) const { return in; }
+  __host__ __device__ const void* epi_ptr(int) const { return nullptr; }
+  __host__ __device__ bool in_active(int) const { return true; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const { lds_vec<double, VZ>(R.p[0], z, a.a); }
   __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int z) const { a.a = lds1<double, double>(R.p[0], z); }
   __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
@@ -923,9 +923,9 @@ struct ApplyOp : G, PassBase {
   static constexpr int NIN = 1, NE = 0;
   static constexpr int in_esz(int) { return 8; }
   static constexpr int epi_esz(int) { return 1; }
-  __device__ const void* in_ptr(int) const { return in; }
-  __device__ const void* epi_ptr(int) const { return nullptr; }
-  __device__ bool in_active(int) const { return true; }
+  __host__ __device__ const void* in_ptr(int) const { return in; }
+  __host__ __device__ const void* epi_ptr(int) const { return nullptr; }
+  __host__ __device__ bool in_active(int) const { return true; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const { lds_vec<double, VZ>(R.p[0], z, a.a); }
   __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int z) const { a.a = lds1<double, CT>(R.p[0], z); }
   __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}

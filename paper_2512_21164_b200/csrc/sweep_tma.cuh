@@ -68,6 +68,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(b))
       : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// GADI_L2PF > 0: the producer also prefetches the rows of plane xp + L2PF
+// into L2 (more DRAM requests in flight than the stage ring holds)
+#ifndef GADI_L2PF
+#define GADI_L2PF 0
+#endif
+#ifndef GADI_SPLITCOPY
+#define GADI_SPLITCOPY 0  // experiment: two bulk copies per input row
+#endif
 __device__ __forceinline__ void consumer_sync(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
@@ -259,8 +270,18 @@ __device__ __forceinline__ void produce_stages(const P& p, const SweepGeom& g, u
             const int a = max(zt0 - hz, 0), b = min(zt0 + TZ + hz, g.nz);  // = in_e0 / in_bytes (j is runtime here)
             const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
             const long long e0 = (long long)xp * g.plane + (long long)yy * g.nz + a;
+#if GADI_SPLITCOPY
+            {
+              const int h = ((b - a) / 2) & ~(16 / esz - 1);
+              bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j) + (a - (zt0 - hz)) * esz, base + e0 * esz,
+                       (unsigned)(h * esz), &full[st]);
+              bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j) + (a + h - (zt0 - hz)) * esz, base + (e0 + h) * esz,
+                       (unsigned)((b - a - h) * esz), &full[st]);
+            }
+#else
             bulk_g2s(sb + TS::off_in(j) + r * TS::rb_in(j) + (a - (zt0 - hz)) * esz, base + e0 * esz,
                      (unsigned)((b - a) * esz), &full[st]);
+#endif
           } else if (ev) {
             const int q2 = q - NIN * (TY + 2);
             const int j = q2 / TY, r = q2 % TY;
@@ -274,6 +295,33 @@ __device__ __forceinline__ void produce_stages(const P& p, const SweepGeom& g, u
           }
         }
       }
+#if GADI_L2PF > 0
+      {
+        const int xq = xp + GADI_L2PF;
+        if (xq <= xb && xq >= -g.hlo && xq < g.nx + g.hhi) {
+          const bool eq = xq >= xa && xq < xb;
+          for (int q = lane; q < NCOPY; q += 32) {
+            if (q < NIN * (TY + 2)) {
+              const int j = q / (TY + 2), yy = y0 - 1 + q % (TY + 2);
+              if (!p.in_active(j) || yy < 0 || yy >= g.ny) continue;
+              const int esz = P::in_esz(j), hz = TS::hz(esz);
+              const int a = max(zt0 - hz, 0), b = min(zt0 + TZ + hz, g.nz);
+              const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
+              bulk_prefetch_l2(base + ((long long)xq * g.plane + (long long)yy * g.nz + a) * esz,
+                               (unsigned)((b - a) * esz));
+            } else if (eq) {
+              const int q2 = q - NIN * (TY + 2);
+              const int j = q2 / TY, yy = y0 + q2 % TY;
+              if (yy >= g.ny) continue;
+              const int esz = P::epi_esz(j);
+              const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
+              bulk_prefetch_l2(base + ((long long)xq * g.plane + (long long)yy * g.nz + zt0) * esz,
+                               (unsigned)((min(zt0 + TZ, g.nz) - zt0) * esz));
+            }
+          }
+        }
+      }
+#endif
     }
   }
 }

@@ -15,6 +15,7 @@
 // the f-plane form cost in issue slots.
 #pragma once
 #include "sweep_tma.cuh"
+#include "tmap.cuh"
 
 namespace gadi {
 
@@ -47,10 +48,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// address of element 0 of row r of input j in stage st
+// address of element 0 (of the tile core) of row r of input j in stage st,
+// as seen by lane tz (tensor-map layout: the lane's box)
 template <class P, class TS>
-__device__ __forceinline__ unsigned char* stage_in_row(unsigned char* stages, int st, int j, int r) {
-  return stages + (size_t)st * TS::STAGE + TS::off_in(j) + r * TS::rb_in(j) + TS::hz(P::in_esz(j)) * P::in_esz(j);
+__device__ __forceinline__ unsigned char* stage_in_row(unsigned char* stages, int st, int j, int r, int tz) {
+  return TS::in_row_ptr(stages, st, j, r, tz);
 }
 
 // field of one lane's VZ-vector at row r of stage st (zeros unless ok)
@@ -64,7 +66,7 @@ __device__ __forceinline__ void stage_fields(const P& p, unsigned char* stages, 
 #pragma unroll
     for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
 #pragma unroll
-    for (int j = 0; j < P::NIN; ++j) R.p[j] = stage_in_row<P, TS>(stages, st, j, r);
+    for (int j = 0; j < P::NIN; ++j) R.p[j] = stage_in_row<P, TS>(stages, st, j, r, zo / VZ);
     typename P::Raw a;
     p.load_raw_sm(a, R, zo);
     p.field_vec(a, f);
@@ -97,10 +99,10 @@ __device__ void inplace_halo_rows(const P& p, const SweepGeom& g, unsigned char*
       if (x >= xa && x < xb) {
         CT f[1][VZ];
         stage_fields<P, TS>(p, stages, slot, 0, lane * VZ, top_ok, f);
-        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, 0)), lane * VZ, VZ,
-                          f[0], true);
+        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, 0, lane)), lane * VZ,
+                          VZ, f[0], true);
         stage_fields<P, TS>(p, stages, slot, TY + 1, lane * VZ, bot_ok, f);
-        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, TY + 1)),
+        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, TY + 1, lane)),
                           lane * VZ, VZ, f[0], true);
         fence_proxy_async_smem();
       }
@@ -123,19 +125,54 @@ struct Tma2Threads {
   static constexpr int value = P::NT + 32 + (HasInplace<P>::value ? 32 : 0);
 };
 
-template <class P>
+// Stage layouts: TM = false, rows of (TZ + 2 hz) elements per input (the
+// row-copy producer); TM = true, the tensor-map boxes of tmap.cuh, each box
+// 128-byte aligned.
+template <class P, bool TM = false>
 struct TmaShape2 : TmaShape<P> {
   using Base = TmaShape<P>;
+  using BX = TmBox<P, Base>;
+  static constexpr int TZ = Base::TZ, TY = Base::TY;
+  static constexpr int r128(int b) { return (b + 127) / 128 * 128; }
+  static constexpr int boxb(int j) { return r128((TY + 2) * BX::BW(j) * P::in_esz(j)); }
+  static constexpr int off_in_tm(int j) {
+    int o = 0;
+    for (int i = 0; i < j; ++i) o += BX::NB(i) * boxb(i);
+    return o;
+  }
+  static constexpr int off_epi_tm(int j) {
+    int o = off_in_tm(P::NIN);
+    for (int i = 0; i < j; ++i) o += r128(TY * TZ * P::epi_esz(i));
+    return o;
+  }
+  static constexpr int STAGE = TM ? r128(off_epi_tm(P::NE)) : Base::STAGE;
+  static constexpr int in_box_off(int j, int k) { return off_in_tm(j) + k * boxb(j); }
+  static __device__ __forceinline__ unsigned char* in_row_ptr(unsigned char* stages, int st, int j, int r, int tz) {
+    const int esz = P::in_esz(j), hz = Base::hz(esz);
+    unsigned char* sb = stages + (size_t)st * STAGE;
+    if constexpr (TM) {
+      const int k = (BX::NB(j) == 2 && tz >= 16) ? 1 : 0;
+      return sb + in_box_off(j, k) + r * BX::BW(j) * esz + (hz - k * BX::BW(j)) * esz;
+    } else {
+      return sb + Base::off_in(j) + r * Base::rb_in(j) + hz * esz;
+    }
+  }
+  static __device__ __forceinline__ unsigned char* epi_row_ptr(unsigned char* stages, int st, int j, int r) {
+    unsigned char* sb = stages + (size_t)st * STAGE;
+    if constexpr (TM) return sb + off_epi_tm(j) + r * TZ * P::epi_esz(j);
+    else return sb + Base::off_epi(j) + r * Base::rb_epi(j);
+  }
   static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : GADI_TMA_BUDGET1_KB) * 1024;
-  static constexpr int NST_RAW = BUDGET / Base::STAGE;
+  static constexpr int NST_RAW = BUDGET / STAGE;
   static constexpr int NST = NST_RAW < 2 ? 2 : (NST_RAW > 12 ? 12 : NST_RAW);
-  static constexpr size_t SMEM = (size_t)NST * Base::STAGE + 3 * NST * sizeof(uint64_t);
+  static constexpr size_t SMEM = (size_t)NST * STAGE + 3 * NST * sizeof(uint64_t);
 };
 
-template <class P>
-__global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB) sweep_tma2_kernel(P p) {
+template <class P, bool TM>
+__global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
+    sweep_tma2_kernel(P p, const __grid_constant__ TmParam<TM> tm) {
   using S = SweepShape<P>;
-  using TS = TmaShape2<P>;
+  using TS = TmaShape2<P, TM>;
   using CT = typename P::CT;
   constexpr int VZ = S::VZ, BZ = S::BZ, BY = S::BY, ZS = S::ZS, NF = S::NF;
   constexpr int TZ = S::TZ, TY = S::TY;
@@ -170,7 +207,10 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB) sweep_tma2_ker
     for (int i = blockIdx.x * (NT + 32) + tid; i < g.nx; i += gridDim.x * (NT + 32)) p.wave_clear[i] = 0u;
 
   if (tid >= NT + (INPL ? 32 : 0)) {
-    produce_stages<P, TS, !GADI_EPI_LDG>(p, g, stages, full, empty, lane);
+    if constexpr (TM)
+      produce_stages_tm<P, TS>(p, g, stages, full, empty, lane, tm);
+    else
+      produce_stages<P, TS, !GADI_EPI_LDG>(p, g, stages, full, empty, lane);
   } else if (INPL && tid >= NT) {
     if constexpr (INPL) inplace_halo_rows<P, TS>(p, g, stages, full, empty, fdone, lane);
   } else {
@@ -188,21 +228,18 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB) sweep_tma2_ker
     };
     auto in_row = [&](int st, int r) {
       SmRow R;
-      const unsigned char* sb = stages + (size_t)st * TS::STAGE;
 #pragma unroll
       for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
 #pragma unroll
-      for (int j = 0; j < NIN; ++j)
-        R.p[j] = sb + TS::off_in(j) + r * TS::rb_in(j) + TS::hz(P::in_esz(j)) * P::in_esz(j);
+      for (int j = 0; j < NIN; ++j) R.p[j] = TS::in_row_ptr(stages, st, j, r, tz);
       return R;
     };
     auto epi_row = [&](int st, int r) {
       SmRow R;
-      const unsigned char* sb = stages + (size_t)st * TS::STAGE;
 #pragma unroll
       for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
 #pragma unroll
-      for (int j = 0; j < NE; ++j) R.p[j] = sb + TS::off_epi(j) + r * TS::rb_epi(j);
+      for (int j = 0; j < NE; ++j) R.p[j] = TS::epi_row_ptr(stages, st, j, r);
       return R;
     };
     // fields of this lane's vector in stage row r; zeros unless valid (nv == VZ)
@@ -248,7 +285,7 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB) sweep_tma2_ker
     auto put_field = [&](int st, const CT (&f)[NF][VZ]) {
       if constexpr (INPL) {
         using ST = typename P::ST;
-        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, st, P::FIELD_IN, ty + 1)), tz * VZ, VZ,
+        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, st, P::FIELD_IN, ty + 1, tz)), tz * VZ, VZ,
                           f[0], true);
         fence_proxy_async_smem();
         __syncwarp();
@@ -299,8 +336,8 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB) sweep_tma2_ker
         if constexpr (INPL) {
           // neighbours' fields of plane x (written one plane ago)
           mbar_wait(&fdone[s], ps.ph);
-          lds_vec<typename P::ST, VZ>(stage_in_row<P, TS>(stages, s, P::FIELD_IN, ty), tz * VZ, fym[0]);
-          lds_vec<typename P::ST, VZ>(stage_in_row<P, TS>(stages, s, P::FIELD_IN, ty + 2), tz * VZ, fyp[0]);
+          lds_vec<typename P::ST, VZ>(stage_in_row<P, TS>(stages, s, P::FIELD_IN, ty, tz), tz * VZ, fym[0]);
+          lds_vec<typename P::ST, VZ>(stage_in_row<P, TS>(stages, s, P::FIELD_IN, ty + 2, tz), tz * VZ, fyp[0]);
         } else {
           fields_at(s, ty, ym_ok, fym);
           fields_at(s, ty + 2, yp_ok, fyp);

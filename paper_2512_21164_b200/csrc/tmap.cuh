@@ -1,0 +1,164 @@
+// TMA tensor-map loads for the barrier-free 3-D sweeps (sweep_tma2.cuh).
+//
+// The row-copy producer issues one cp.async.bulk per stage row and input
+// (20 for HcgA, 26 for HcgB per plane of a 256 x 8 tile), and the measured
+// pass time follows the number of bulk copies per stage (splitting every
+// input row into two copies: HcgA 232 -> 328 us, profiles/tiling_r01.md).
+// With a 3-D tensor map per vector the whole (TY+2)-row haloed tile of an
+// input is one or two box loads (box width <= 256 elements: 2 x 136 bf16 /
+// fp16, 1 x 136 fp32, 1 x 68 fp64) and an epilogue tile one box, so a stage
+// is 3-5 loads; rows and columns outside the grid (y-halo at the domain
+// edge, z-pads at the first and last tile, planes beyond the slab) arrive
+// zero-filled by the hardware.  The maps are encoded on the host
+// (cuTensorMapEncodeTiled through the runtime's driver entry point, cached
+// per buffer in the context) and passed by value as a __grid_constant__
+// kernel parameter, so CUDA-graph capture records them with the launch.
+//
+// Shared-memory layout of an input with two boxes: box k holds elements
+// [k*W/2, (k+1)*W/2) of each of the TY+2 rows, W = TZ + 2*hz; lanes 0-15 of
+// a row read box 0 and lanes 16-31 box 1 (their z-edge pads included), so a
+// lane's row base pointer selects its box once.
+#pragma once
+#include <cuda.h>
+#include "sweep_tma.cuh"
+
+namespace gadi {
+
+struct TmapSet {
+  CUtensorMap in[4];
+  CUtensorMap epi[4];
+  int ok;
+};
+struct TmapNone {  // the row-copy instances take no maps (keeps their parameter block small)
+  int ok;
+};
+template <bool TM>
+using TmParam = typename std::conditional<TM, TmapSet, TmapNone>::type;
+
+// compile-time eligibility: 3-D tiles of 32 lanes per row, and passes with
+// at least two haloed inputs (HcgA, CgnrP1).  Measured per pass (cd3d 512^3
+// bf16, us): HcgA 232 -> 207, CgnrP1 199 -> 181 with tensor maps, but HcgB
+// 262 -> 275-280 and CgnrP2 / CgnrInit / CgnrP3 slower too: for a single
+// haloed input the ten parallel row copies finish a stage sooner than its
+// two box loads (profiles/tiling_r01.md)
+template <class P>
+struct TmaTm {
+  static constexpr bool value = SweepShape<P>::BZ == 32 && SweepShape<P>::BY > 1 && P::NIN >= 2;
+};
+
+template <class P, class TS>
+struct TmBox {
+  static constexpr int W(int j) { return TS::TZ + 2 * TS::hz(P::in_esz(j)); }
+  static constexpr int NB(int j) { return W(j) > 256 ? 2 : 1; }
+  static constexpr int BW(int j) { return W(j) / NB(j); }
+};
+
+#ifndef GADI_TM_EVICT_FIRST
+#define GADI_TM_EVICT_FIRST 0
+#endif
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+#if GADI_TM_EVICT_FIRST
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+  return;
+#endif
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// GADI_TM_EPI = 1: the epilogue-only inputs (no halo) also load as one box
+// per stage; 0: as one bulk row copy per row (lanes in parallel) into the
+// same dense [TY][TZ] layout
+#ifndef GADI_TM_EPI
+#define GADI_TM_EPI 0
+#endif
+
+// Producer warp, tensor-map form: same ring protocol and plane sequence as
+// produce_stages (sweep_tma.cuh); lane 0 posts the byte count (whole boxes,
+// zero-filled parts included) and issues the loads.
+template <class P, class TS, bool EPI = true>
+__device__ __forceinline__ void produce_stages_tm(const P& p, const SweepGeom& g, unsigned char* stages,
+                                                  uint64_t* full, uint64_t* empty, int lane, const TmapSet& tm) {
+  constexpr int TZ = TS::TZ, TY = TS::TY, NIN = P::NIN, NE = EPI ? P::NE : 0, NST = TS::NST;
+  using B = TmBox<P, TS>;
+  SegIter it(g, gridDim.x, blockIdx.x);
+  int tile, xa, xb;
+  int gs = 0, slot = 0, round = 0;
+  while (it.next(tile, xa, xb)) {
+    const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
+    for (int xp = xa - 1; xp <= xb; ++xp, ++gs) {
+      const int st = slot;
+      if (gs >= NST) mbar_wait(&empty[st], (unsigned)((round - 1) & 1));
+      if (++slot == NST) {
+        slot = 0;
+        ++round;
+      }
+      if (p.wave && xp - p.wlead >= 0) {
+        if (lane == 0) {
+          const volatile unsigned* cnt = p.wave + (xp - p.wlead);
+          while (*cnt < gridDim.x) __nanosleep(100);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        unsigned char* sb = stages + (size_t)st * TS::STAGE;
+        const bool pv = (xp >= -g.hlo && xp < g.nx + g.hhi);
+        const bool ev = pv && xp >= xa && xp < xb;
+        unsigned bytes = 0;
+        if (pv) {
+#pragma unroll
+          for (int j = 0; j < NIN; ++j)
+            if (p.in_active(j)) bytes += (unsigned)((TY + 2) * B::W(j) * P::in_esz(j));
+          if (ev) {
+#pragma unroll
+            for (int j = 0; j < NE; ++j)
+              bytes += (unsigned)((GADI_TM_EPI ? TY : min(TY, g.ny - y0)) * (min(zt0 + TZ, g.nz) - zt0) *
+                                  P::epi_esz(j));
+          }
+        }
+        mbar_expect_tx(&full[st], bytes);
+        if (pv) {
+          const int xc = xp + g.hlo;  // the maps start at the lowest valid plane
+#pragma unroll
+          for (int j = 0; j < NIN; ++j) {
+            if (!p.in_active(j)) continue;
+            const int hz = TS::hz(P::in_esz(j));
+#pragma unroll
+            for (int k = 0; k < B::NB(j); ++k)
+              tma_load_3d(sb + TS::in_box_off(j, k), &tm.in[j], zt0 - hz + k * B::BW(j), y0 - 1, xc, &full[st]);
+          }
+#if GADI_TM_EPI
+          if (ev) {
+#pragma unroll
+            for (int j = 0; j < NE; ++j) tma_load_3d(sb + TS::off_epi_tm(j), &tm.epi[j], zt0, y0, xc, &full[st]);
+          }
+#endif
+        }
+      }
+      __syncwarp();
+#if !GADI_TM_EPI
+      if (NE > 0 && xp >= xa && xp < xb) {
+        unsigned char* sb = stages + (size_t)st * TS::STAGE;
+        for (int q = lane; q < NE * TY; q += 32) {
+          const int j = q / TY, r = q % TY, yy = y0 + r;
+          if (yy >= g.ny) continue;
+          const int esz = P::epi_esz(j);
+          const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
+          bulk_g2s(sb + TS::off_epi_tm(j) + r * TZ * esz, base + ((long long)xp * g.plane + (long long)yy * g.nz + zt0) * esz,
+                   (unsigned)((min(zt0 + TZ, g.nz) - zt0) * esz), &full[st]);
+        }
+      }
+#endif
+    }
+  }
+}
+
+}  // namespace gadi
