@@ -113,7 +113,8 @@ struct Ctx {
   // TMA tensor maps of the 3-D sweeps (tmap.cuh), encoded once per
   // (buffer, element size, box); tmap = 0 (GADI_TMAP=0) keeps row copies
   int tmap = 1;
-  int tm_promo = 3;  // CUtensorMapL2promotion (GADI_TM_PROMO): 0 none, 1 64B, 2 128B, 3 256B
+  // CUtensorMapL2promotion (GADI_TM_PROMO): 0 none, 1 64B (measured best: HcgA 205 -> 197 us vs 256B), 2 128B, 3 256B
+  int tm_promo = 1;
   void* tm_encode = nullptr;
   std::map<std::array<long long, 4>, CUtensorMap> tmcache;
   cudaGraph_t graph_h = nullptr, graph_s = nullptr;
