@@ -66,17 +66,17 @@ inline bool tm_map(Ctx* c, const void* ptr, int esz, int bw, int bh, CUtensorMap
   return true;
 }
 
-template <class P>
+template <class P, int TM>
 inline bool tm_fill(Ctx* c, const P& p, TmapSet& tm) {
-  using TS = TmaShape2<P, true>;
+  using TS = TmaShape2<P, TM>;
   using BX = TmBox<P, TmaShape<P>>;
   if (c->ndim != 3 || ((long long)c->ny * c->nz) % 16) return false;
   for (int j = 0; j < P::NIN; ++j) {
-    if (!p.in_active(j)) continue;
+    if (!p.in_active(j) || TM != 1) continue;
     if ((uintptr_t)p.in_ptr(j) % 16 || !tm_map(c, p.in_ptr(j), P::in_esz(j), BX::BW(j), TS::TY + 2, &tm.in[j]))
       return false;
   }
-  for (int j = 0; j < P::NE; ++j)
+  for (int j = 0; j < P::NE && TM == 2; ++j)
     if ((uintptr_t)p.epi_ptr(j) % 16 || !tm_map(c, p.epi_ptr(j), P::epi_esz(j), TS::TZ, TS::TY, &tm.epi[j]))
       return false;
   return true;
@@ -122,25 +122,29 @@ inline int launch_sweep(Ctx* c, P& p) {
     // evenly among them (SegIter).  Barrier-free consumers (sweep_tma2.cuh)
     // unless GADI_TMA2=0 selects the f-plane form (sweep_tma.cuh).
     const bool v2 = c->tma2 != 0 && TmaForm2<P>::value;
-    // tensor-map producer for the 3-D barrier-free passes (tmap.cuh)
+    // tensor-map producer for the 3-D barrier-free passes (tmap.cuh): mode 1
+    // boxes for two haloed inputs, mode 2 boxes for the epilogue inputs
+    constexpr int TMM = TmaTm<P>::value ? 1 : (TmaTmEpi<P>::value ? 2 : 0);
     TmapSet tm;
     tm.ok = 0;
-    if constexpr (TmaTm<P>::value) {
-      if (v2 && c->tmap) tm.ok = tm_fill<P>(c, p, tm) ? 1 : 0;
+    if constexpr (TMM != 0) {
+      if (v2 && c->tmap) tm.ok = tm_fill<P, TMM>(c, p, tm) ? 1 : 0;
     }
-    const size_t smem = v2 ? (tm.ok ? TmaShape2<P, true>::SMEM : TmaShape2<P>::SMEM) : TmaShape<P>::SMEM;
+    const size_t smem = v2 ? (tm.ok ? TmaShape2<P, TMM>::SMEM : TmaShape2<P>::SMEM) : TmaShape<P>::SMEM;
     const int NTH = v2 ? Tma2Threads<P>::value : TmaThreads<P>::NTOT;
     static int occ1 = 0, occ2 = 0, occ3 = 0;
     int& occ = v2 ? (tm.ok ? occ3 : occ2) : occ1;
     if (!occ) {
       if (v2 && tm.ok) {
-        GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P, true>, NTH, smem));
+        if constexpr (TMM != 0) {
+          GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P, TMM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+          GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P, TMM>, NTH, smem));
+        }
       } else if (v2) {
-        GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P, false>, NTH, smem));
+        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P, 0>, NTH, smem));
       } else {
         GADI_CUDA(cudaFuncSetAttribute(sweep_tma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma_kernel<P>, NTH, smem));
@@ -156,7 +160,7 @@ inline int launch_sweep(Ctx* c, P& p) {
       nbl = tiles;  // one CTA per tile through all planes (SegIter with nblocks == tiles)
       p.wave = c->wavecnt + (size_t)c->wpar * c->nx;
       p.wave_clear = c->wavecnt + (size_t)(c->wpar ^ 1) * c->nx;
-      p.wlead = (v2 ? (tm.ok ? TmaShape2<P, true>::NST : TmaShape2<P>::NST) : TmaShape<P>::NST) + 4;
+      p.wlead = (v2 ? (tm.ok ? TmaShape2<P, TMM>::NST : TmaShape2<P>::NST) : TmaShape<P>::NST) + 4;
       c->wpar ^= 1;
     }
     if (c->lockstep && tiles <= slots) {
@@ -168,10 +172,11 @@ inline int launch_sweep(Ctx* c, P& p) {
     const int nb = (int)nbl;
     if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
     prof_begin(c, P::KID);
-    if (v2 && tm.ok)
-      sweep_tma2_kernel<P, true><<<nb, NTH, smem, c->stream>>>(p, tm);
-    else if (v2)
-      sweep_tma2_kernel<P, false><<<nb, NTH, smem, c->stream>>>(p, TmapNone{0});
+    if (v2 && tm.ok) {
+      if constexpr (TMM != 0) sweep_tma2_kernel<P, TMM><<<nb, NTH, smem, c->stream>>>(p, tm);
+    } else if (v2) {
+      sweep_tma2_kernel<P, 0><<<nb, NTH, smem, c->stream>>>(p, TmapNone{0});
+    }
     else
       sweep_tma_kernel<P><<<nb, NTH, smem, c->stream>>>(p);
     prof_end(c);

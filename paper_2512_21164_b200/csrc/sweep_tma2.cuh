@@ -128,7 +128,7 @@ struct Tma2Threads {
 // Stage layouts: TM = false, rows of (TZ + 2 hz) elements per input (the
 // row-copy producer); TM = true, the tensor-map boxes of tmap.cuh, each box
 // 128-byte aligned.
-template <class P, bool TM = false>
+template <class P, int TM = 0>
 struct TmaShape2 : TmaShape<P> {
   using Base = TmaShape<P>;
   using BX = TmBox<P, Base>;
@@ -141,7 +141,7 @@ struct TmaShape2 : TmaShape<P> {
     return o;
   }
   static constexpr int off_epi_tm(int j) {
-    int o = off_in_tm(P::NIN);
+    int o = TM == 1 ? off_in_tm(P::NIN) : r128(Base::off_in(P::NIN));
     for (int i = 0; i < j; ++i) o += r128(TY * TZ * P::epi_esz(i));
     return o;
   }
@@ -150,7 +150,7 @@ struct TmaShape2 : TmaShape<P> {
   static __device__ __forceinline__ unsigned char* in_row_ptr(unsigned char* stages, int st, int j, int r, int tz) {
     const int esz = P::in_esz(j), hz = Base::hz(esz);
     unsigned char* sb = stages + (size_t)st * STAGE;
-    if constexpr (TM) {
+    if constexpr (TM == 1) {
       const int k = (BX::NB(j) == 2 && tz >= 16) ? 1 : 0;
       return sb + in_box_off(j, k) + r * BX::BW(j) * esz + (hz - k * BX::BW(j)) * esz;
     } else {
@@ -168,7 +168,7 @@ struct TmaShape2 : TmaShape<P> {
   static constexpr size_t SMEM = (size_t)NST * STAGE + 3 * NST * sizeof(uint64_t);
 };
 
-template <class P, bool TM>
+template <class P, int TM>
 __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
     sweep_tma2_kernel(P p, const __grid_constant__ TmParam<TM> tm) {
   using S = SweepShape<P>;
@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
     for (int i = blockIdx.x * (NT + 32) + tid; i < g.nx; i += gridDim.x * (NT + 32)) p.wave_clear[i] = 0u;
 
   if (tid >= NT + (INPL ? 32 : 0)) {
-    if constexpr (TM)
-      produce_stages_tm<P, TS>(p, g, stages, full, empty, lane, tm);
+    if constexpr (TM != 0)
+      produce_stages_tm<P, TS, TM>(p, g, stages, full, empty, lane, tm);
     else
       produce_stages<P, TS, !GADI_EPI_LDG>(p, g, stages, full, empty, lane);
   } else if (INPL && tid >= NT) {

@@ -32,8 +32,8 @@ struct TmapSet {
 struct TmapNone {  // the row-copy instances take no maps (keeps their parameter block small)
   int ok;
 };
-template <bool TM>
-using TmParam = typename std::conditional<TM, TmapSet, TmapNone>::type;
+template <int TM>
+using TmParam = typename std::conditional<TM != 0, TmapSet, TmapNone>::type;
 
 // compile-time eligibility: 3-D tiles of 32 lanes per row, and passes with
 // at least two haloed inputs (HcgA, CgnrP1).  Measured per pass (cd3d 512^3
@@ -44,6 +44,17 @@ using TmParam = typename std::conditional<TM, TmapSet, TmapNone>::type;
 template <class P>
 struct TmaTm {
   static constexpr bool value = SweepShape<P>::BZ == 32 && SweepShape<P>::BY > 1 && P::NIN >= 2;
+};
+// GADI_TM_EPIBOX = 1: the other 3-D passes with epilogue inputs load those
+// as one box each (TM = 2).  Measured: HcgB 263 -> 271 us, CgnrP2 280 ->
+// 277 us -- off by default.
+#ifndef GADI_TM_EPIBOX
+#define GADI_TM_EPIBOX 0
+#endif
+template <class P>
+struct TmaTmEpi {
+  static constexpr bool value =
+      GADI_TM_EPIBOX && SweepShape<P>::BZ == 32 && SweepShape<P>::BY > 1 && !TmaTm<P>::value && P::NE > 0;
 };
 
 template <class P, class TS>
@@ -74,20 +85,17 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// GADI_TM_EPI = 1: the epilogue-only inputs (no halo) also load as one box
-// per stage; 0: as one bulk row copy per row (lanes in parallel) into the
-// same dense [TY][TZ] layout
-#ifndef GADI_TM_EPI
-#define GADI_TM_EPI 0
-#endif
-
-// Producer warp, tensor-map form: same ring protocol and plane sequence as
-// produce_stages (sweep_tma.cuh); lane 0 posts the byte count (whole boxes,
-// zero-filled parts included) and issues the loads.
-template <class P, class TS, bool EPI = true>
+// Producer warp with tensor maps.  TM = 1: the haloed inputs load as boxes
+// (lane 0) and the epilogue inputs as bulk row copies (lanes in parallel);
+// TM = 2: the haloed inputs as row copies and each epilogue input as one
+// [TY][TZ] box.  Same ring protocol and plane sequence as produce_stages
+// (sweep_tma.cuh); lane 0 posts the stage's byte count (whole boxes, their
+// zero-filled parts included; row copies clipped to the grid) first.
+template <class P, class TS, int TM>
 __device__ __forceinline__ void produce_stages_tm(const P& p, const SweepGeom& g, unsigned char* stages,
                                                   uint64_t* full, uint64_t* empty, int lane, const TmapSet& tm) {
-  constexpr int TZ = TS::TZ, TY = TS::TY, NIN = P::NIN, NE = EPI ? P::NE : 0, NST = TS::NST;
+  constexpr int TZ = TS::TZ, TY = TS::TY, NIN = P::NIN, NE = P::NE, NST = TS::NST;
+  constexpr int NRC = TM == 1 ? NE * TY : NIN * (TY + 2);  // row copies per stage
   using B = TmBox<P, TS>;
   SegIter it(g, gridDim.x, blockIdx.x);
   int tile, xa, xb;
@@ -108,55 +116,70 @@ __device__ __forceinline__ void produce_stages_tm(const P& p, const SweepGeom& g
         }
         __syncwarp();
       }
+      const bool pv = (xp >= -g.hlo && xp < g.nx + g.hhi);
+      const bool ev = pv && xp >= xa && xp < xb;
+      const int xc = xp + g.hlo;  // the maps start at the lowest valid plane
+      const int nyv = min(TY, g.ny - y0);                  // valid epilogue rows
+      const int ylo = max(y0 - 1, 0), yhi = min(y0 + TY + 1, g.ny);  // valid haloed rows
       if (lane == 0) {
-        unsigned char* sb = stages + (size_t)st * TS::STAGE;
-        const bool pv = (xp >= -g.hlo && xp < g.nx + g.hhi);
-        const bool ev = pv && xp >= xa && xp < xb;
         unsigned bytes = 0;
         if (pv) {
 #pragma unroll
-          for (int j = 0; j < NIN; ++j)
-            if (p.in_active(j)) bytes += (unsigned)((TY + 2) * B::W(j) * P::in_esz(j));
+          for (int j = 0; j < NIN; ++j) {
+            if (!p.in_active(j)) continue;
+            const int esz = P::in_esz(j), hz = TS::hz(esz);
+            if (TM == 1)
+              bytes += (unsigned)((TY + 2) * B::W(j) * esz);
+            else
+              bytes += (unsigned)((yhi - ylo) * (min(zt0 + TZ + hz, g.nz) - max(zt0 - hz, 0)) * esz);
+          }
           if (ev) {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
-              bytes += (unsigned)((GADI_TM_EPI ? TY : min(TY, g.ny - y0)) * (min(zt0 + TZ, g.nz) - zt0) *
-                                  P::epi_esz(j));
+              bytes += (unsigned)((TM == 2 ? TY : nyv) * (TM == 2 ? TZ : min(zt0 + TZ, g.nz) - zt0) * P::epi_esz(j));
           }
         }
         mbar_expect_tx(&full[st], bytes);
-        if (pv) {
-          const int xc = xp + g.hlo;  // the maps start at the lowest valid plane
+        if (pv && TM == 1) {
 #pragma unroll
           for (int j = 0; j < NIN; ++j) {
             if (!p.in_active(j)) continue;
             const int hz = TS::hz(P::in_esz(j));
 #pragma unroll
             for (int k = 0; k < B::NB(j); ++k)
-              tma_load_3d(sb + TS::in_box_off(j, k), &tm.in[j], zt0 - hz + k * B::BW(j), y0 - 1, xc, &full[st]);
+              tma_load_3d(stages + (size_t)st * TS::STAGE + TS::in_box_off(j, k), &tm.in[j], zt0 - hz + k * B::BW(j),
+                          y0 - 1, xc, &full[st]);
           }
-#if GADI_TM_EPI
-          if (ev) {
+        }
+        if (ev && TM == 2) {
 #pragma unroll
-            for (int j = 0; j < NE; ++j) tma_load_3d(sb + TS::off_epi_tm(j), &tm.epi[j], zt0, y0, xc, &full[st]);
-          }
-#endif
+          for (int j = 0; j < NE; ++j) tma_load_3d(TS::epi_row_ptr(stages, st, j, 0), &tm.epi[j], zt0, y0, xc, &full[st]);
         }
       }
       __syncwarp();
-#if !GADI_TM_EPI
-      if (NE > 0 && xp >= xa && xp < xb) {
-        unsigned char* sb = stages + (size_t)st * TS::STAGE;
-        for (int q = lane; q < NE * TY; q += 32) {
-          const int j = q / TY, r = q % TY, yy = y0 + r;
-          if (yy >= g.ny) continue;
-          const int esz = P::epi_esz(j);
-          const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
-          bulk_g2s(sb + TS::off_epi_tm(j) + r * TZ * esz, base + ((long long)xp * g.plane + (long long)yy * g.nz + zt0) * esz,
-                   (unsigned)((min(zt0 + TZ, g.nz) - zt0) * esz), &full[st]);
+      // row copies, one per lane
+      if (TM == 1 ? ev : pv) {
+        for (int q = lane; q < NRC; q += 32) {
+          if constexpr (TM == 1) {
+            const int j = q / TY, yy = y0 + q % TY;
+            if (yy >= g.ny) continue;
+            const int esz = P::epi_esz(j);
+            const unsigned char* base = reinterpret_cast<const unsigned char*>(p.epi_ptr(j));
+            bulk_g2s(TS::epi_row_ptr(stages, st, j, q % TY),
+                     base + ((long long)xp * g.plane + (long long)yy * g.nz + zt0) * esz,
+                     (unsigned)((min(zt0 + TZ, g.nz) - zt0) * esz), &full[st]);
+          } else {
+            const int j = q / (TY + 2), r = q % (TY + 2), yy = y0 - 1 + r;
+            if (!p.in_active(j) || yy < 0 || yy >= g.ny) continue;
+            const int esz = P::in_esz(j), hz = TS::hz(esz);
+            const int a = max(zt0 - hz, 0), b = min(zt0 + TZ + hz, g.nz);
+            const unsigned char* base = reinterpret_cast<const unsigned char*>(p.in_ptr(j));
+            bulk_g2s(TS::in_row_ptr(stages, st, j, r, 0) + (a - zt0) * esz,
+                     base + ((long long)xp * g.plane + (long long)yy * g.nz + a) * esz, (unsigned)((b - a) * esz),
+                     &full[st]);
+          }
         }
       }
-#endif
     }
   }
 }
