@@ -102,3 +102,19 @@ def test_fullsize_inner_solve(gpu, big, us, true_bound):
     assert st.converged and st.iterations > 10 and st.final_relative_residual <= 1e-3
     assert np.all(np.isfinite(z))
     assert st.true_relative_residual < true_bound, st.true_relative_residual
+
+
+@pytest.mark.parametrize("fam", ["cd3d", "crd"])
+def test_host_stager_roundtrip(gpu, fam):
+    """Vectors of >= 128 MiB cross the ABI through the pinned chunk stager
+    (csrc/hostcopy.cu); sizes that are not a multiple of the 32 MiB chunk
+    and the complex family's block <-> interleaved permutation round-trip
+    bit for bit, and into a freshly allocated destination."""
+    from paper_2512_21164_b200.stencil import spec_complex_rd
+    spec = g.build_cd_3d(262).A.spec if fam == "cd3d" else spec_complex_rd(3001)
+    assert spec.n * 8 >= 128 << 20 and (spec.n * 8) % (32 << 20)
+    rng = np.random.default_rng(1)
+    b = rng.standard_normal(spec.n)
+    with device.open_context(device.make_desc(spec, 1.0, "fp64")) as ctx:
+        ctx.set_rhs(b)
+        assert np.array_equal(ctx.get_rhs(), b)
