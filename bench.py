@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--outer-tol", type=float, default=1e-12)
     ap.add_argument("--inner-tol", type=float, default=1e-2)
     ap.add_argument("--outer-maxit", type=int, default=2000)
+    ap.add_argument("--rounding", choices=["storage", "reference"], default="storage",
+                    help="inner-solver arithmetic (gadi_solve rounding=): the storage model or the reference's "
+                         "per-operation rounding in the fused passes")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-ng", type=int, default=128, help="grid of the bounded CPU sample")
@@ -226,7 +229,7 @@ def run_ours(a, rank, world):
 
     def solve(timer=None, problem=None, return_x=False, c=cfg):
         p = problem if problem is not None else build(a.ng)
-        return g.gadi_solve(p, cfg=c, device=dev, return_x=return_x, hooks=timer, comm=comm)
+        return g.gadi_solve(p, cfg=c, device=dev, return_x=return_x, hooks=timer, comm=comm, rounding=a.rounding)
 
     for _ in range(a.warmup):
         solve()

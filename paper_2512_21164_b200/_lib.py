@@ -296,7 +296,7 @@ class Context:
         check(self._L.gadi_set_rounding(self.h, int(mode), FMT_CODES[dot_fmt]))
 
     KERNELS = ["hcg_init", "hcg_a", "hcg_b", "cgnr_init", "cgnr_p1", "cgnr_p2", "cgnr_p3",
-               "crd_init", "crd_p1", "crd_p2", "outer", "norm_a", "norm_b", "apply"]
+               "crd_init", "crd_p1", "crd_p2", "outer", "norm_a", "norm_b", "apply", "dot_tree"]
 
     def prof_enable(self, on=True):
         check(self._L.gadi_prof_enable(self.h, 1 if on else 0))

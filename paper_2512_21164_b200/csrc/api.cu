@@ -5,7 +5,10 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include "engine.cuh"
 #include "norm_fused.cuh"
 #include "hostcopy.h"
@@ -16,6 +19,25 @@ static thread_local std::string g_err;
 int set_error(const std::string& msg, int code) {
   g_err = msg;
   return code;
+}
+
+int kernel_occupancy(const void* fn, int device, int nthreads, size_t smem, bool carveout, int* occ) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({fn, device});
+  if (it != cache.end()) {
+    *occ = it->second;
+    return 0;
+  }
+  if (smem > 48 * 1024) GADI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (carveout) GADI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int o = 0;
+  GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, nthreads, smem));
+  if (o < 1) o = 1;
+  cache[{fn, device}] = o;
+  *occ = o;
+  return 0;
 }
 
 static size_t fmt_bytes(int f) {
@@ -127,14 +149,8 @@ static int norm_fused_step(Ctx* c, const double* in, double* out) {
   p.outv = out;
   p.A = c->A;
   p.AT = c->AT;
-  static int occ = 0;
-  if (!occ) {
-    GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)S::SMEM));
-    GADI_CUDA(cudaFuncSetAttribute(norm_fused_kernel<DIM, DENSE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, norm_fused_kernel<DIM, DENSE>, S::NTOT, S::SMEM));
-    if (occ < 1) occ = 1;
-  }
+  int occ = 1;
+  GADI_TRY(occupancy_of(c, norm_fused_kernel<DIM, DENSE>, S::NTOT, S::SMEM, &occ, true));
   p.g = make_geom(c, S::TZ, S::TY, S::VZ, (long long)occ * c->sms);
   const long long units = (long long)p.g.nzt * p.g.nyt * p.g.nx;
   const int nb = (int)std::min<long long>(units, (long long)occ * c->sms * c->waves);
@@ -182,7 +198,8 @@ static void free_ctx(Ctx* c) {
       if (p) cudaFree(p);
     m = CsrDev();
   }
-  void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst, c->gbuf, c->wavecnt};
+  void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst, c->gbuf, c->wavecnt,
+                c->tree, c->tlvl, c->tticket, c->taux};
   for (void* p : sp)
     if (p) cudaFree(p);
   void* hp[] = {c->h_hst, c->h_sst, c->h_osum, c->h_nst};
@@ -667,7 +684,7 @@ int gadi_outer_step(gadi_ctx* h, const gadi_step_args* a, gadi_outer_scalars* ou
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   GADI_CUDA(cudaEventRecord(c->ev[0], c->stream));
-  if (c->rounding) {
+  if (c->rounding == 2) {
     GADI_TRY(exact_h_solve(c, c->r, a->scale, a->inner_tol, a->maxit_h));
     GADI_CUDA(cudaEventRecord(c->ev[1], c->stream));
     GADI_TRY(exact_s_solve(c, c->ex[EX_Z], a->coeff, a->inner_tol, a->maxit_s));
@@ -710,7 +727,7 @@ int gadi_h_solve(gadi_ctx* h, const double* rhs, double tol, int maxit, double* 
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   GADI_TRY(upload(c, rhs, c->r));
-  if (c->rounding) {
+  if (c->rounding == 2) {
     GADI_TRY(exact_h_solve(c, c->r, 1.0, tol, maxit));
     GADI_TRY(download(c, c->ex[EX_Z], x));
   } else {
@@ -727,7 +744,7 @@ int gadi_s_solve(gadi_ctx* h, const double* rhs, double tol, int maxit, double* 
   Ctx* c = &h->c;
   GADI_CUDA(cudaSetDevice(c->device));
   GADI_TRY(upload(c, rhs, c->r));
-  if (c->rounding) {
+  if (c->rounding == 2) {
     GADI_TRY(exact_s_solve(c, c->r, 1.0, tol, maxit));
     GADI_TRY(download(c, c->ex[EX_Y], x));
   } else {
@@ -810,13 +827,40 @@ int gadi_timer_stop(gadi_ctx* h, double* ms) {
 
 int gadi_set_rounding(gadi_ctx* h, int mode, int dot_fmt) {
   Ctx* c = &h->c;
-  if (mode != 0 && mode != 1) return set_error("rounding mode must be 0 (storage) or 1 (reference)", GADI_ERR_ARG);
+  if (mode < 0 || mode > 2)
+    return set_error("rounding mode must be 0 (storage), 1 (reference, fused) or 2 (reference, per operation)",
+                     GADI_ERR_ARG);
   if (dot_fmt < GADI_BF16 || dot_fmt > GADI_FP64) return set_error("bad dot format", GADI_ERR_ARG);
   GADI_CUDA(cudaSetDevice(c->device));
-  if (mode == 1 && c->comm) return set_error("reference rounding runs on a single domain", GADI_ERR_UNSUPPORTED);
-  c->rounding = (mode == 1 && c->us != GADI_FP64) ? 1 : 0;  // fp64 inner arithmetic is already exact
+  if (mode != 0 && c->comm) return set_error("reference rounding runs on a single domain", GADI_ERR_UNSUPPORTED);
+  // the fused reference passes cover the stencil families; general CSR
+  // operators (and u_s = fp64, whose per-operation emulation is not needed
+  // for mode 2) keep the per-operation path
+  if (mode == 1 && c->kind == GADI_CSR) mode = c->us == GADI_FP64 ? 0 : 2;
+  if (mode == 2 && c->us == GADI_FP64) mode = 0;
+  if (mode != c->graph_mode) {  // loop graphs were captured with the other passes
+    GADI_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->gexec_h) cudaGraphExecDestroy(c->gexec_h);
+    if (c->gexec_s) cudaGraphExecDestroy(c->gexec_s);
+    if (c->graph_h) cudaGraphDestroy(c->graph_h);
+    if (c->graph_s) cudaGraphDestroy(c->graph_s);
+    c->gexec_h = c->gexec_s = nullptr;
+    c->graph_h = c->graph_s = nullptr;
+    c->graph_mode = mode;
+  }
+  c->rounding = mode;
   c->dot_fmt = dot_fmt;
-  if (c->rounding) return exact_alloc(c);
+  c->dk = dot_fmt == GADI_BF16 ? DK_BF16 : (dot_fmt == GADI_FP16 ? DK_F16 : DK_F32);
+  if (mode == 2) return exact_alloc(c);
+  if (mode == 1 && !c->tree) {
+    const long long lv = 2 * ((c->n + TF_BLK - 1) / TF_BLK) + 64;
+    GADI_CUDA(cudaMalloc((void**)&c->tree, sizeof(float) * (size_t)(c->n + 64)));
+    GADI_CUDA(cudaMalloc((void**)&c->tlvl, sizeof(float) * (size_t)lv));
+    GADI_CUDA(cudaMalloc((void**)&c->tticket, sizeof(unsigned int)));
+    GADI_CUDA(cudaMalloc((void**)&c->taux, 8 * sizeof(double)));
+    GADI_CUDA(cudaMemsetAsync(c->tticket, 0, sizeof(unsigned int), c->stream));
+    GADI_CUDA(cudaMemsetAsync(c->taux, 0, 8 * sizeof(double), c->stream));
+  }
   return 0;
 }
 

@@ -118,6 +118,7 @@ struct Ctx {
   void* tm_encode = nullptr;
   std::map<std::array<long long, 4>, CUtensorMap> tmcache;
   cudaGraph_t graph_h = nullptr, graph_s = nullptr;
+  int graph_mode = -1;  // rounding mode the loop graphs were captured with
   cudaGraphExec_t gexec_h = nullptr, gexec_s = nullptr;
   unsigned* wavecnt = nullptr;  // 2 x nx per-plane counters (alternating parity)
   int wpar = 0;
@@ -134,10 +135,19 @@ struct Ctx {
   double prof_ms[K_NKID] = {};
   long long prof_n[K_NKID] = {};
 
-  // inner-solver arithmetic: 0 storage model (engine.cuh), 1 the reference's
-  // per-operation rounding emulation (exact.cu) with dot accumulation format
+  // inner-solver arithmetic: 0 storage model (engine.cuh); 1 the reference's
+  // per-operation rounding inside the fused passes (strict.cuh); 2 the same
+  // emulation host-driven per operation (exact.cu: CSR operators, and a
+  // cross-check of mode 1).  dot_fmt: the reference's fl_dot format.
   int rounding = 0, dot_fmt = GADI_FP64;
   double* ex[EX_N] = {};
+  // mode 1: fl_dot leaves, the finisher's level buffer / ticket, the passes'
+  // fp64 totals handed to the finisher
+  float* tree = nullptr;
+  float* tlvl = nullptr;
+  unsigned int* tticket = nullptr;
+  double* taux = nullptr;
+  int dk = 0;  // DotKind of dot_fmt
   CsrDev csr[CS_N];
 
   CoefT<double> A, AT, H, S, ST;
@@ -146,6 +156,16 @@ struct Ctx {
 };
 
 int set_error(const std::string& msg, int code);
+
+// Per-(kernel, device) launch setup: the dynamic shared-memory opt-in applies
+// to the device current when it is set, so it is made once per device (and
+// the resulting occupancy cached) under a lock -- slab ranks may run as
+// threads of one process (SlabComm.local).
+int kernel_occupancy(const void* fn, int device, int nthreads, size_t smem, bool carveout, int* occ);
+template <class K>
+inline int occupancy_of(Ctx* c, K* kernel, int nthreads, size_t smem, int* occ, bool carveout = false) {
+  return kernel_occupancy(reinterpret_cast<const void*>(kernel), c->device, nthreads, smem, carveout, occ);
+}
 
 #define GADI_CUDA(call)                                                                   \
   do {                                                                                    \

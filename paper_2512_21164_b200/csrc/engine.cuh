@@ -109,6 +109,38 @@ inline int post_reduce(Ctx* c, const P& p) {
 
 inline double* defer_row(Ctx* c) { return c->comm ? c->gbuf + (size_t)c->comm->rank * GROW : nullptr; }
 
+inline int ilog2(long long v) {
+  int l = 0;
+  while ((1LL << (l + 1)) <= v) ++l;
+  return l;
+}
+
+// Reference rounding: after a pass that wrote fl_dot leaves, sum them and run
+// its scalar recurrence (tree_finish_kernel, strict.cuh).
+template <class P>
+inline int launch_tree(Ctx* c, const P& p, long long leaves) {
+  const long long nb = std::max(1LL, (leaves + TF_BLK - 1) / TF_BLK);
+  prof_begin(c, K_TREE);
+  tree_finish_kernel<P><<<(int)nb, TF_NT, 0, c->stream>>>(p, leaves, c->tlvl, c->tticket);
+  prof_end(c);
+  c->launches++;
+  GADI_CUDA(cudaGetLastError());
+  return 0;
+}
+template <class P>
+inline void tree_setup(Ctx* c, P& p) {
+  p.tout = TreeOut{nullptr, -1, 0, nullptr, 0};
+  if constexpr (TreeSlot<P>::value >= 0)
+    p.tout = TreeOut{c->tree, -1, c->dk, c->taux, c->kind == GADI_COMPLEX ? c->n / 2 : 0};
+}
+// leaves of one dot: one per element, else one per aligned block (two per
+// block of an interleaved complex vector: the real and imaginary halves)
+inline long long tree_leaves(const Ctx* c, const TreeOut& t) {
+  if (t.tlog < 0) return c->n;
+  if (t.cm) return 2 * (t.cm >> (t.tlog - 1));
+  return (c->n + (1LL << t.tlog) - 1) >> t.tlog;
+}
+
 template <class P>
 inline int launch_sweep(Ctx* c, P& p) {
   using S = SweepShape<P>;
@@ -117,6 +149,7 @@ inline int launch_sweep(Ctx* c, P& p) {
   p.defer = defer_row(c);
   p.wave = p.wave_clear = nullptr;
   p.wlead = 0;
+  tree_setup(c, p);
   if (tma_aligned<P>(c)) {
     // one resident wave of CTAs; the kernel splits the (tile, plane) units
     // evenly among them (SegIter).  Barrier-free consumers (sweep_tma2.cuh)
@@ -132,24 +165,21 @@ inline int launch_sweep(Ctx* c, P& p) {
     }
     const size_t smem = v2 ? (tm.ok ? TmaShape2<P, TMM>::SMEM : TmaShape2<P>::SMEM) : TmaShape<P>::SMEM;
     const int NTH = v2 ? Tma2Threads<P>::value : TmaThreads<P>::NTOT;
-    static int occ1 = 0, occ2 = 0, occ3 = 0;
-    int& occ = v2 ? (tm.ok ? occ3 : occ2) : occ1;
-    if (!occ) {
-      if (v2 && tm.ok) {
-        if constexpr (TMM != 0) {
-          GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P, TMM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-          GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P, TMM>, NTH, smem));
-        }
-      } else if (v2) {
-        GADI_CUDA(cudaFuncSetAttribute(sweep_tma2_kernel<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma2_kernel<P, 0>, NTH, smem));
-      } else {
-        GADI_CUDA(cudaFuncSetAttribute(sweep_tma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        GADI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_tma_kernel<P>, NTH, smem));
+    int occ = 1;
+    if (v2 && tm.ok) {
+      if constexpr (TMM != 0) GADI_TRY(occupancy_of(c, sweep_tma2_kernel<P, TMM>, NTH, smem, &occ));
+    } else if (v2) {
+      GADI_TRY(occupancy_of(c, sweep_tma2_kernel<P, 0>, NTH, smem, &occ));
+    } else {
+      GADI_TRY(occupancy_of(c, sweep_tma_kernel<P>, NTH, smem, &occ));
+    }
+    // reference rounding on the barrier-free form: one fl_dot leaf per
+    // aligned block of G = min(2^v2(nz), 32 VZ) elements (strict.cuh)
+    if constexpr (TreeSlot<P>::value >= 0) {
+      if (v2) {
+        const int a = c->nz & -c->nz, gb = std::min(a, 32 * P::VZ);
+        if (gb >= P::VZ) p.tout.tlog = ilog2(gb);
       }
-      if (occ < 1) occ = 1;
     }
     p.g = make_geom(c, S::TZ, S::TY, P::VZ, (long long)occ * c->sms);
     const long long tiles = (long long)p.g.nzt * p.g.nyt;
@@ -186,11 +216,8 @@ inline int launch_sweep(Ctx* c, P& p) {
     if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
     const size_t smem = S::SMEM;
     if (smem > 48 * 1024) {
-      static bool attr = false;
-      if (!attr) {
-        GADI_CUDA(cudaFuncSetAttribute(sweep_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-      }
+      int occ = 1;
+      GADI_TRY(occupancy_of(c, sweep_kernel<P>, P::NT, smem, &occ));
     }
     prof_begin(c, P::KID);
     sweep_kernel<P><<<nb, P::NT, smem, c->stream>>>(p);
@@ -198,7 +225,9 @@ inline int launch_sweep(Ctx* c, P& p) {
   }
   c->launches++;
   GADI_CUDA(cudaGetLastError());
-  return post_reduce(c, p);
+  GADI_TRY(post_reduce(c, p));
+  if constexpr (TreeSlot<P>::value >= 0) GADI_TRY(launch_tree(c, p, tree_leaves(c, p.tout)));
+  return 0;
 }
 
 template <class P>
@@ -208,6 +237,11 @@ inline int launch_pw(Ctx* c, P& p) {
   p.ticket = c->ticket;
   p.pstride = c->pstride;
   p.defer = defer_row(c);
+  tree_setup(c, p);
+  if constexpr (TreeSlot<P>::value >= 0) {
+    p.tout.tlog = ilog2(32 * P::VZ);
+    if (p.tout.cm && p.tout.cm % (16 * P::VZ)) p.tout.tlog = -1;  // halves not block-aligned
+  }
   const long long chunks = (c->n + (long long)PW_NT * P::VZ - 1) / ((long long)PW_NT * P::VZ);
   int nb = (int)std::min<long long>(chunks, (long long)c->sms * 8);
   nb = std::max(nb, 1);
@@ -216,7 +250,9 @@ inline int launch_pw(Ctx* c, P& p) {
   prof_end(c);
   c->launches++;
   GADI_CUDA(cudaGetLastError());
-  return post_reduce(c, p);
+  GADI_TRY(post_reduce(c, p));
+  if constexpr (TreeSlot<P>::value >= 0) GADI_TRY(launch_tree(c, p, tree_leaves(c, p.tout)));
+  return 0;
 }
 
 
@@ -442,10 +478,11 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ H-solve (CG)
-  template <int DIM, int ZS>
+  // RF: the reference's per-operation rounding (strict.cuh), else the storage model
+  template <int DIM, int ZS, bool RF>
   static int h_solve_t(Ctx* c, double scale, double tol, int maxit) {
     typedef GeoT<ST, DIM, ZS> G;
-    HcgInit<ST> hi;
+    HcgInit<ST, RF> hi;
     hi.r64 = c->r;
     hi.rs = (ST*)c->R;
     hi.z = (ST*)c->Z;
@@ -459,7 +496,7 @@ struct Engine {
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
     auto iter = [&](int k) -> int {
         if (k == 0) {
-          HcgA<G, true> a;
+          HcgA<G, true, RF> a;
           a.st = c->hst;
           a.r = (const ST*)c->R;
           a.pin = P[0];
@@ -467,7 +504,7 @@ struct Engine {
           a.H = H;
           GADI_TRY(launch_sweep(c, a));
         } else {
-          HcgA<G> a;
+          HcgA<G, false, RF> a;
           a.st = c->hst;
           a.r = (const ST*)c->R;
           a.pin = P[k & 1];
@@ -476,7 +513,7 @@ struct Engine {
           GADI_TRY(launch_sweep(c, a));
         }
         GADI_TRY(halo(c, P[(k + 1) & 1], sizeof(ST)));
-        HcgB<G> b;
+        HcgB<G, RF> b;
         b.st = c->hst;
         b.p = P[(k + 1) & 1];
         b.z = (ST*)c->Z;
@@ -500,11 +537,11 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ S-solve (CGNR)
-  template <int DIM>
+  template <int DIM, bool RF>
   static int s_solve_real(Ctx* c, double coeff, double tol, int maxit) {
     typedef GeoT<ST, DIM, 1> G;
     const CoefT<CT> S = cast_coef<CT>(c->S), STc = cast_coef<CT>(c->ST);
-    CgnrInit<G> ci;
+    CgnrInit<G, RF> ci;
     ci.st = c->sst;
     ci.z = (const ST*)c->Z;
     ci.r = (ST*)c->R;
@@ -519,7 +556,7 @@ struct Engine {
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
     auto iter = [&](int k) -> int {
         if (k == 0) {
-          CgnrP1<G, true> p1;
+          CgnrP1<G, true, RF> p1;
           p1.st = c->sst;
           p1.rbar = (const ST*)c->RB;
           p1.pin = P[0];
@@ -527,7 +564,7 @@ struct Engine {
           p1.S = S;
           GADI_TRY(launch_sweep(c, p1));
         } else {
-          CgnrP1<G> p1;
+          CgnrP1<G, false, RF> p1;
           p1.st = c->sst;
           p1.rbar = (const ST*)c->RB;
           p1.pin = P[k & 1];
@@ -536,7 +573,7 @@ struct Engine {
           GADI_TRY(launch_sweep(c, p1));
         }
         GADI_TRY(halo(c, P[(k + 1) & 1], sizeof(ST)));
-        CgnrP2<G> p2;
+        CgnrP2<G, RF> p2;
         p2.st = c->sst;
         p2.p = P[(k + 1) & 1];
         p2.y = (ST*)c->Y;
@@ -544,7 +581,7 @@ struct Engine {
         p2.S = S;
         GADI_TRY(launch_sweep(c, p2));
         GADI_TRY(halo(c, c->R, sizeof(ST)));
-        CgnrP3<G> p3;
+        CgnrP3<G, RF> p3;
         p3.st = c->sst;
         p3.r = (const ST*)c->R;
         p3.rbar = (ST*)c->RB;
@@ -566,9 +603,10 @@ struct Engine {
     return halo(c, c->Y, sizeof(ST));  // y is a field input of the outer pass
   }
 
+  template <bool RF>
   static int s_solve_cplx(Ctx* c, double coeff, double tol, int maxit) {
     const CT al = (CT)c->d.alpha_s;
-    CInit<ST> ci;
+    CInit<ST, RF> ci;
     ci.vs = (const ST*)c->VS;
     ci.al = al;
     ci.z = (const ST*)c->Z;
@@ -580,14 +618,14 @@ struct Engine {
     ci.maxit = maxit;
     GADI_TRY(launch_pw(c, ci));
     auto iter = [&](int) -> int {
-        CP1<ST> p1;
+        CP1<ST, RF> p1;
         p1.vs = (const ST*)c->VS;
         p1.al = al;
         p1.r = (const ST*)c->R;
         p1.p = (ST*)c->P[0];
         p1.st = c->sst;
         GADI_TRY(launch_pw(c, p1));
-        CP2<ST> p2;
+        CP2<ST, RF> p2;
         p2.vs = (const ST*)c->VS;
         p2.al = al;
         p2.p = (const ST*)c->P[0];
@@ -666,18 +704,26 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ vtable
+  template <bool RF>
+  static int h_solve_m(Ctx* c, double scale, double tol, int maxit) {
+    if (c->kind == GADI_COMPLEX)
+      return c->ndim == 3 ? h_solve_t<3, 2, RF>(c, scale, tol, maxit) : h_solve_t<2, 2, RF>(c, scale, tol, maxit);
+    if (c->ndim == 3) return h_solve_t<3, 1, RF>(c, scale, tol, maxit);
+    return h_solve_t<2, 1, RF>(c, scale, tol, maxit);
+  }
   static int h_solve(Ctx* c, double scale, double tol, int maxit) {
     if (c->kind == GADI_CSR) return h_solve_csr(c, scale, tol, maxit);
-    if (c->kind == GADI_COMPLEX)
-      return c->ndim == 3 ? h_solve_t<3, 2>(c, scale, tol, maxit) : h_solve_t<2, 2>(c, scale, tol, maxit);
-    if (c->ndim == 3) return h_solve_t<3, 1>(c, scale, tol, maxit);
-    return h_solve_t<2, 1>(c, scale, tol, maxit);
+    return c->rounding == 1 ? h_solve_m<true>(c, scale, tol, maxit) : h_solve_m<false>(c, scale, tol, maxit);
+  }
+  template <bool RF>
+  static int s_solve_m(Ctx* c, double coeff, double tol, int maxit) {
+    if (c->kind == GADI_COMPLEX) return s_solve_cplx<RF>(c, coeff, tol, maxit);
+    if (c->ndim == 3) return s_solve_real<3, RF>(c, coeff, tol, maxit);
+    return s_solve_real<2, RF>(c, coeff, tol, maxit);
   }
   static int s_solve(Ctx* c, double coeff, double tol, int maxit) {
     if (c->kind == GADI_CSR) return s_solve_csr(c, coeff, tol, maxit);
-    if (c->kind == GADI_COMPLEX) return s_solve_cplx(c, coeff, tol, maxit);
-    if (c->ndim == 3) return s_solve_real<3>(c, coeff, tol, maxit);
-    return s_solve_real<2>(c, coeff, tol, maxit);
+    return c->rounding == 1 ? s_solve_m<true>(c, coeff, tol, maxit) : s_solve_m<false>(c, coeff, tol, maxit);
   }
   static int outer(Ctx* c, double scale, int has_e) {
     if (c->kind == GADI_CSR) return outer_csr(c, scale, has_e);

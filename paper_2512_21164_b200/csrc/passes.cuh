@@ -20,6 +20,7 @@
 // the reference's ordered (non-FMA) stencil arithmetic.
 #pragma once
 #include "sweep_tma2.cuh"
+#include "strict.cuh"
 
 namespace gadi {
 
@@ -62,13 +63,16 @@ struct GeoT {
 // Kernel ids for the live per-kernel timers (gadi_prof_*).
 enum KernelId {
   K_HCG_INIT = 0, K_HCG_A, K_HCG_B, K_CGNR_INIT, K_CGNR_P1, K_CGNR_P2, K_CGNR_P3,
-  K_C_INIT, K_C_P1, K_C_P2, K_OUTER, K_NORM_A, K_NORM_B, K_APPLY, K_NKID
+  K_C_INIT, K_C_P1, K_C_P2, K_OUTER, K_NORM_A, K_NORM_B, K_APPLY, K_TREE, K_NKID
 };
 
 struct InnerState {
   double rs, nrhs, alpha, beta, relres, tol;
   int it, maxit, done, converged, breakdown, pad;
 };
+// Reference rounding (strict.cuh) of a pass's scalars: RndCode<ST> when the
+// pass runs the reference's per-operation emulation, else 0 (fp64 scalars).
+template <class ST, bool RF> struct ScalarRnd { static constexpr int value = RF ? RndCode<ST>::value : 0; };
 
 struct OuterSums {
   // 0 sum r_mon^2, 1 max|r_alg|, 2 sum r_alg^2, 3 sum x^2, 4 sum e^2, 5 sum (A e)^2
@@ -84,15 +88,15 @@ struct NormState {
 // The device-side scalar logic of the inner solvers, shared by the stencil
 // passes below, the CSR passes (csr.cuh) and the slab finalize kernel.
 // cg_spd (inner.py:67-86):
-__device__ __forceinline__ void fin_cg_alpha(InnerState* st, double php) {
+__device__ __forceinline__ void fin_cg_alpha(InnerState* st, double php, int rnd = 0) {
   if (php <= 0.0) {  // inner.py:70-72 breakdown
     st->breakdown = 1;
     st->done = 1;
     return;
   }
-  st->alpha = st->rs / php;
+  st->alpha = sround(st->rs / php, rnd);  // inner.py:73 fl_op("div", rs, php, fmt)
 }
-__device__ __forceinline__ void fin_cg_beta(InnerState* st, double rs_new) {
+__device__ __forceinline__ void fin_cg_beta(InnerState* st, double rs_new, int rnd = 0) {
   const int it = st->it + 1;
   st->it = it;
   const double relres = sqrt(fmax(rs_new, 0.0)) / st->nrhs;  // inner.py:78
@@ -106,7 +110,7 @@ __device__ __forceinline__ void fin_cg_beta(InnerState* st, double rs_new) {
     st->done = 1;
     return;
   }
-  st->beta = rs_new / st->rs;
+  st->beta = sround(rs_new / st->rs, rnd);  // inner.py:84
   st->rs = rs_new;
   if (it >= st->maxit) st->done = 1;
 }
@@ -131,13 +135,13 @@ __device__ __forceinline__ void fin_cgnr_init(InnerState* st, double rs, double 
     st->done = 1;
   }
 }
-__device__ __forceinline__ void fin_cgnr_alpha(InnerState* st, double denom) {
+__device__ __forceinline__ void fin_cgnr_alpha(InnerState* st, double denom, int rnd = 0) {
   if (denom <= 0.0) {  // inner.py:123-125
     st->breakdown = 1;
     st->done = 1;
     return;
   }
-  st->alpha = st->rs / denom;
+  st->alpha = sround(st->rs / denom, rnd);  // inner.py:126
 }
 __device__ __forceinline__ void fin_cgnr_relres(InnerState* st, double rr) {
   const int it = st->it + 1;
@@ -151,12 +155,12 @@ __device__ __forceinline__ void fin_cgnr_relres(InnerState* st, double rr) {
   }
   if (it >= st->maxit) st->done = 1;
 }
-__device__ __forceinline__ void fin_cgnr_beta(InnerState* st, double rs_new) {
+__device__ __forceinline__ void fin_cgnr_beta(InnerState* st, double rs_new, int rnd = 0) {
   if (rs_new <= 0.0) {  // inner.py:136-137
     st->done = 1;
     return;
   }
-  st->beta = rs_new / st->rs;
+  st->beta = sround(rs_new / st->rs, rnd);  // inner.py:138
   st->rs = rs_new;
 }
 // matrix_norm_2 (analysis.py:58-69), after w = A^T A v and ||w||^2
@@ -223,7 +227,14 @@ __device__ __forceinline__ void stencil_vec_any(const CoefT<CT>& c, const CT (&x
   __device__ void stencil_vec(int, const CT (&xm)[G::VZ], const CT (&ym)[G::VZ], const CT (&ce)[G::VZ],     \
                               const CT (&lf)[G::ZS], const CT (&rt)[G::ZS], const CT (&yp)[G::VZ],          \
                               const CT (&xp)[G::VZ], CT (&out)[G::VZ]) const {                              \
-    stencil_vec_any<ORD, (G::BY > 1), G::VZ, G::ZS>(COEF, xm, ym, ce, lf, rt, yp, xp, out);                  \
+    if constexpr (RF)                                                                                       \
+      stencil_vec_ref<ST, (G::BY > 1), G::VZ, G::ZS>(COEF, xm, ym, ce, lf, rt, yp, xp, out);                \
+    else                                                                                                    \
+      stencil_vec_any<ORD, (G::BY > 1), G::VZ, G::ZS>(COEF, xm, ym, ce, lf, rt, yp, xp, out);               \
+  }                                                                                                         \
+  __device__ CT stencil1(const CoefT<CT>& cf, const Nb<CT>& n) const {                                      \
+    if constexpr (RF) return stencil_ref1<ST>(cf, n);                                                       \
+    else return apply_stencil<ORD>(cf, CT(0), n);                                                           \
   }
 
 // y[k] = round(c + s * a[k]) (axpy rounded to storage) on a whole vector,
@@ -242,6 +253,19 @@ __device__ __forceinline__ void axpy_round(CT s, const CT (&a)[VZ], const CT (&c
 #pragma unroll
     for (int k = 0; k < VZ; ++k) y[k] = round_to<ST>(fma_rn(s, a[k], c[k]));
   }
+}
+
+// axpy of either model: the reference's fl(c + fl(s a)) (RF), or the
+// storage model's fused fp32 multiply-add rounded once to u_s
+template <class ST, bool RF, int VZ, class CT>
+__device__ __forceinline__ void axpy_m(CT s, const CT (&a)[VZ], const CT (&c)[VZ], CT (&y)[VZ]) {
+  if constexpr (RF) axpy_ref<ST>(s, a, c, y);
+  else axpy_round<ST>(s, a, c, y);
+}
+template <class ST, bool RF, class CT>
+__device__ __forceinline__ CT axpy_m1(CT s, CT a, CT c) {
+  if constexpr (RF) return axpy_ref1<ST>(s, a, c);
+  else return round_to<ST>(fma_rn(s, a, c));
 }
 
 // The stencil output of the storage model is a u_s vector (the paper's
@@ -263,6 +287,17 @@ __device__ __forceinline__ void round_vec(const CT (&a)[VZ], CT (&o)[VZ]) {
   }
 }
 
+// RF: the reference-rounded stencil output is already on the u_s grid
+template <class ST, bool RF, int VZ, class CT>
+__device__ __forceinline__ void round_vec_m(const CT (&a)[VZ], CT (&o)[VZ]) {
+  if constexpr (RF) {
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) o[k] = a[k];
+  } else {
+    round_vec<ST>(a, o);
+  }
+}
+
 // Common plumbing every pass carries.
 struct PassBase {
   SweepGeom g;
@@ -276,16 +311,20 @@ struct PassBase {
   double* defer;  // slab decomposition: this rank's row of the gather buffer
   double* partials;
   unsigned int* ticket;
+  TreeOut tout;   // reference rounding: fl_dot leaves (strict.cuh)
 };
 
 // ============================================================== H-CG passes
 // f = (it == 0) ? r : round(r + beta p_in) ; Hf ; store p_out ; sum f.Hf
-template <class G, bool FIRST = false>
+// RF (all CG / CGNR passes): the reference's per-operation rounding
+// (strict.cuh) instead of the storage model; TS is the pass's fl_dot slot.
+template <class G, bool FIRST = false, bool RF = false>
 struct HcgA : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int TS = (RF && !ORD) ? 0 : -1;
   static constexpr int KID = K_HCG_A;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
@@ -311,7 +350,7 @@ struct HcgA : G, PassBase {
 #pragma unroll
       for (int k = 0; k < G::VZ; ++k) f[0][k] = a.r[k];
     } else {
-      axpy_round<ST>(beta, a.p, a.r, f[0]);
+      axpy_m<ST, RF>(beta, a.p, a.r, f[0]);
     }
   }
   GADI_STENCIL_VEC(H)
@@ -338,30 +377,35 @@ struct HcgA : G, PassBase {
     a.r = cvt_in<CT>(r[i]);
     a.p = first ? CT(0) : cvt_in<CT>(pin[i]);
   }
-  __device__ CT fval(CT rv, CT pv) const { return first ? rv : round_to<ST>(fma_rn(beta, pv, rv)); }
+  __device__ CT fval(CT rv, CT pv) const { return first ? rv : axpy_m1<ST, RF>(beta, pv, rv); }
   __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = fval(a.r[k], first ? CT(0) : a.p[k]); }
   __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = fval(a.r, a.p); }
   __device__ void load_epi(Epi&, long long, int) const {}
   __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
-    return apply_stencil<ORD>(H, CT(0), n);
+    return stencil1(H, n);
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
     store_any<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
-    CT hp[G::VZ];
-    round_vec<ST>(s[0], hp);
-    red[0] += dotv<CT, G::VZ>(fc[0], hp, nv);
+    if constexpr (TS >= 0) {
+      red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, fc[0], s[0]);  // fl_dot(p, Hp, dfmt), inner.py:69
+    } else {
+      CT hp[G::VZ];
+      round_vec<ST>(s[0], hp);
+      red[0] += dotv<CT, G::VZ>(fc[0], hp, nv);
+    }
   }
-  __device__ void finalize(const double (&t)[1]) const { fin_cg_alpha(st, t[0]); }
+  __device__ void finalize(const double (&t)[1]) const { fin_cg_alpha(st, t[0], ScalarRnd<ST, RF>::value); }
 };
 
 // f = p ; Hp ; z += alpha p ; r -= alpha Hp ; sum r.r ; convergence, beta
-template <class G>
+template <class G, bool RF = false>
 struct HcgB : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int TS = (RF && !ORD) ? 0 : -1;
   static constexpr int KID = K_HCG_B;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
@@ -400,29 +444,31 @@ struct HcgB : G, PassBase {
     load_any<ST, G::VZ, false>(r, i, nv, e.r, g.vec);
   }
   __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
-    return apply_stencil<ORD>(H, CT(0), n);
+    return stencil1(H, n);
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
                            double (&red)[1]) const {
     CT zn[G::VZ], rn[G::VZ], hp[G::VZ];
-    round_vec<ST>(s[0], hp);
-    axpy_round<ST>(alpha, fc[0], e.z, zn);
-    axpy_round<ST>(-alpha, hp, e.r, rn);
-    red[0] += dotv<CT, G::VZ>(rn, rn, nv);
+    round_vec_m<ST, RF>(s[0], hp);
+    axpy_m<ST, RF>(alpha, fc[0], e.z, zn);   // inner.py:74
+    axpy_m<ST, RF>(-alpha, hp, e.r, rn);     // inner.py:75
+    if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rn, rn);  // inner.py:76
+    else red[0] += dotv<CT, G::VZ>(rn, rn, nv);
     store_any<ST, G::VZ>(z, i, nv, zn, g.vec);
     store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
   }
-  __device__ void finalize(const double (&t)[1]) const { fin_cg_beta(st, t[0]); }
+  __device__ void finalize(const double (&t)[1]) const { fin_cg_beta(st, t[0], ScalarRnd<ST, RF>::value); }
 };
 
 // ============================================================== CGNR passes
 // rhs2 = round(coeff z) ; r = rhs2 ; rbar = round(S^T rhs2) ; y = 0
-template <class G>
+template <class G, bool RF = false>
 struct CgnrInit : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 2;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int TS = (RF && !ORD) ? 0 : -1;
   static constexpr int KID = K_CGNR_INIT;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
@@ -450,24 +496,26 @@ struct CgnrInit : G, PassBase {
   __device__ void load_epi_sm(Epi&, const SmRow&, int) const {}
   __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<ST, G::VZ, true>(z, i, nv, a.z, g.vec); }
   __device__ void load_raw_s(RawS& a, long long i) const { a.z = cvt_in<CT>(z[i]); }
-  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = round_to<ST>(coeff * a.z[k]); }
-  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = round_to<ST>(coeff * a.z); }
+  // gadi.py:158 rhs2 = quantize(coeff * z)
+  __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = round_to<ST>(mul_rn(coeff, a.z[k])); }
+  __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = round_to<ST>(mul_rn(coeff, a.z)); }
   __device__ void load_epi(Epi&, long long, int) const {}
   __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
-    return apply_stencil<ORD>(ST_, CT(0), n);
+    return stencil1(ST_, n);
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[2]) const {
     CT rb[G::VZ], zero[G::VZ];
 #pragma unroll
     for (int k = 0; k < G::VZ; ++k) {
-      rb[k] = round_to<ST>(s[0][k]);
+      rb[k] = RF ? s[0][k] : round_to<ST>(s[0][k]);  // RF: already on the u_s grid
       zero[k] = CT(0);
       if (k < nv) {
-        red[0] += (double)(rb[k] * rb[k]);
-        red[1] += (double)fc[0][k] * (double)fc[0][k];
+        if constexpr (TS < 0) red[0] += (double)(rb[k] * rb[k]);
+        red[1] += (double)fc[0][k] * (double)fc[0][k];  // inner.py:108 fp64 ||rhs||
       }
     }
+    if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rb, rb);  // inner.py:116
     store_any<ST, G::VZ>(r, i, nv, fc[0], g.vec);
     store_any<ST, G::VZ>(rbar, i, nv, rb, g.vec);
     store_any<ST, G::VZ>(y, i, nv, zero, g.vec);
@@ -476,12 +524,13 @@ struct CgnrInit : G, PassBase {
 };
 
 // f = (it==0) ? rbar : round(rbar + beta p_in) ; w = S f ; store p_out ; sum w.w
-template <class G, bool FIRST = false>
+template <class G, bool FIRST = false, bool RF = false>
 struct CgnrP1 : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int TS = (RF && !ORD) ? 0 : -1;
   static constexpr int KID = K_CGNR_P1;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
@@ -506,7 +555,7 @@ struct CgnrP1 : G, PassBase {
 #pragma unroll
       for (int k = 0; k < G::VZ; ++k) f[0][k] = a.rb[k];
     } else {
-      axpy_round<ST>(beta, a.p, a.rb, f[0]);
+      axpy_m<ST, RF>(beta, a.p, a.rb, f[0]);  // inner.py:139
     }
   }
   GADI_STENCIL_VEC(S)
@@ -533,25 +582,26 @@ struct CgnrP1 : G, PassBase {
     a.rb = cvt_in<CT>(rbar[i]);
     a.p = first ? CT(0) : cvt_in<CT>(pin[i]);
   }
-  __device__ CT fval(CT rv, CT pv) const { return first ? rv : round_to<ST>(fma_rn(beta, pv, rv)); }
+  __device__ CT fval(CT rv, CT pv) const { return first ? rv : axpy_m1<ST, RF>(beta, pv, rv); }
   __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = fval(a.rb[k], first ? CT(0) : a.p[k]); }
   __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = fval(a.rb, a.p); }
   __device__ void load_epi(Epi&, long long, int) const {}
   __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
-    return apply_stencil<ORD>(S, CT(0), n);
+    return stencil1(S, n);
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
     store_any<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
     CT w[G::VZ];
-    round_vec<ST>(s[0], w);
-    red[0] += dotv<CT, G::VZ>(w, w, nv);
+    round_vec_m<ST, RF>(s[0], w);
+    if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, w, w);  // inner.py:122
+    else red[0] += dotv<CT, G::VZ>(w, w, nv);
   }
-  __device__ void finalize(const double (&t)[1]) const { fin_cgnr_alpha(st, t[0]); }
+  __device__ void finalize(const double (&t)[1]) const { fin_cgnr_alpha(st, t[0], ScalarRnd<ST, RF>::value); }
 };
 
 // f = p ; w = S p ; y += alpha p ; r -= alpha w ; fp64 ||r||^2 ; convergence
-template <class G>
+template <class G, bool RF = false>
 struct CgnrP2 : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
@@ -595,14 +645,14 @@ struct CgnrP2 : G, PassBase {
     load_any<ST, G::VZ, false>(r, i, nv, e.r, g.vec);
   }
   __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
-    return apply_stencil<ORD>(S, CT(0), n);
+    return stencil1(S, n);
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
                            double (&red)[1]) const {
     CT yn[G::VZ], rn[G::VZ], w[G::VZ];
-    round_vec<ST>(s[0], w);
-    axpy_round<ST>(alpha, fc[0], e.y, yn);
-    axpy_round<ST>(-alpha, w, e.r, rn);
+    round_vec_m<ST, RF>(s[0], w);
+    axpy_m<ST, RF>(alpha, fc[0], e.y, yn);  // inner.py:127
+    axpy_m<ST, RF>(-alpha, w, e.r, rn);     // inner.py:128
 #pragma unroll
     for (int k = 0; k < G::VZ; ++k)
       if (k < nv) red[0] += (double)rn[k] * (double)rn[k];
@@ -613,12 +663,13 @@ struct CgnrP2 : G, PassBase {
 };
 
 // rbar = round(S^T r) ; rs_new = rbar.rbar ; beta
-template <class G>
+template <class G, bool RF = false>
 struct CgnrP3 : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
+  static constexpr int TS = (RF && !ORD) ? 0 : -1;
   static constexpr int KID = K_CGNR_P3;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
   InnerState* st;
@@ -645,19 +696,20 @@ struct CgnrP3 : G, PassBase {
   __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = a.r; }
   __device__ void load_epi(Epi&, long long, int) const {}
   __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
-    return apply_stencil<ORD>(ST_, CT(0), n);
+    return stencil1(ST_, n);
   }
   __device__ void epilogue(long long i, int nv, const CT (&)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
     CT rb[G::VZ];
 #pragma unroll
     for (int k = 0; k < G::VZ; ++k) {
-      rb[k] = round_to<ST>(s[0][k]);
+      rb[k] = RF ? s[0][k] : round_to<ST>(s[0][k]);  // RF: already on the u_s grid
     }
-    red[0] += dotv<CT, G::VZ>(rb, rb, nv);
+    if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rb, rb);  // inner.py:135
+    else red[0] += dotv<CT, G::VZ>(rb, rb, nv);
     store_any<ST, G::VZ>(rbar, i, nv, rb, g.vec);
   }
-  __device__ void finalize(const double (&t)[1]) const { fin_cgnr_beta(st, t[0]); }
+  __device__ void finalize(const double (&t)[1]) const { fin_cgnr_beta(st, t[0], ScalarRnd<ST, RF>::value); }
 };
 
 // ============================================================== outer pass
@@ -934,6 +986,22 @@ struct ApplyOp : G, PassBase {
   __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = a.a[k]; }
   __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = a.a; }
   __device__ void load_epi(Epi&, long long, int) const {}
+  // the reference-rounding stencil of the fused passes (strict.cuh) on whole
+  // vectors: gadi_spmv(strict = 1) checks it bitwise against the reference
+  __device__ void stencil_vec(int, const CT (&xm)[VZ], const CT (&ym)[VZ], const CT (&ce)[VZ],
+                              const CT (&lf)[G::ZS], const CT (&rt)[G::ZS], const CT (&yp)[VZ],
+                              const CT (&xp)[VZ], CT (&out)[VZ]) const {
+    if constexpr (STRICT) {
+      stencil_vec_ref<ST, (G::BY > 1), VZ, G::ZS>(C, xm, ym, ce, lf, rt, yp, xp, out);
+    } else {
+#pragma unroll
+      for (int k = 0; k < VZ; ++k) {
+        const CT zm = (k >= G::ZS) ? ce[k - G::ZS] : lf[k];
+        const CT zp = (k + G::ZS < VZ) ? ce[k + G::ZS] : rt[k + G::ZS - VZ];
+        out[k] = apply_stencil<ORD>(C, CT(0), xm[k], ym[k], zm, ce[k], zp, yp[k], xp[k]);
+      }
+    }
+  }
   __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][VZ], const Epi&) const {
     if constexpr (STRICT) {
       const CT cf[7] = {C.lo[0], C.lo[1], C.lo[2], C.d, C.up[2], C.up[1], C.up[0]};

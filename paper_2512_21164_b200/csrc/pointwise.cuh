@@ -18,9 +18,22 @@ __global__ void __launch_bounds__(PW_NT) pointwise_kernel(P p) {
   for (int s = 0; s < NR; ++s) red[s] = 0.0;
   const long long n = p.n;
   const long long step = (long long)gridDim.x * PW_NT * VZ;
-  for (long long i = ((long long)blockIdx.x * PW_NT + threadIdx.x) * VZ; i < n; i += step) {
-    const int nv = (int)((n - i) < VZ ? (n - i) : VZ);
-    p.apply(i, nv, red);
+  if constexpr (TreeSlot<P>::value >= 0) {
+    // reference rounding: warp-uniform trips, one fl_dot leaf per warp vector
+    // block of 32 VZ elements (tout.tlog = log2(32 VZ), strict.cuh)
+    const int lane = threadIdx.x & 31;
+    for (long long w0 = ((long long)blockIdx.x * PW_NT + (threadIdx.x & ~31)) * VZ; w0 < n; w0 += step) {
+      const long long i = w0 + (long long)lane * VZ;
+      const int nv = (int)((n - i) < VZ ? ((n - i) > 0 ? (n - i) : 0) : VZ);
+      if (nv > 0) p.apply(i, nv, red);
+      if (p.tout.tlog >= 0) tree_emit<VZ, 2>(p.tout, i, nv > 0, lane, red[TreeSlot<P>::value]);
+      red[TreeSlot<P>::value] = 0.0;
+    }
+  } else {
+    for (long long i = ((long long)blockIdx.x * PW_NT + threadIdx.x) * VZ; i < n; i += step) {
+      const int nv = (int)((n - i) < VZ ? (n - i) : VZ);
+      p.apply(i, nv, red);
+    }
   }
   if constexpr (P::HAS_RED) {
     double tot[NR];
@@ -39,6 +52,7 @@ struct PwBase {
   double* partials;
   unsigned int* ticket;
   int pstride;
+  TreeOut tout;   // reference rounding: fl_dot leaves (strict.cuh)
 };
 
 __device__ __forceinline__ void init_state(InnerState* st, double tol, int maxit) {
@@ -54,11 +68,12 @@ __device__ __forceinline__ void init_state(InnerState* st, double tol, int maxit
 
 // r_s = RNE_{u_s}(scale * r) (gadi.py:151-153); z = 0; rs = r_s.r_s;
 // nrhs = ||r_s||_2 (fp64; inner.py:56-63) and the zero-rhs short cut.
-template <class ST>
+template <class ST, bool RF = false>
 struct HcgInit : PwBase {
   typedef typename CTOf<ST>::type CT;
   static constexpr int VZ = (int)(16 / sizeof(ST)) >= 2 ? (int)(16 / sizeof(ST)) : 2;
   static constexpr int NR = 2;
+  static constexpr int TS = (RF && !std::is_same<ST, double>::value) ? 0 : -1;
   static constexpr bool HAS_RED = true;
   static constexpr int KID = K_HCG_INIT;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
@@ -78,10 +93,11 @@ struct HcgInit : PwBase {
       f[k] = cvt_in<CT>(Store<ST>::from(scale * rr[k]));
       zero[k] = CT(0);
       if (k < nv) {
-        red[0] += (double)(f[k] * f[k]);
+        if constexpr (TS < 0) red[0] += (double)(f[k] * f[k]);
         red[1] += (double)f[k] * (double)f[k];
       }
     }
+    if constexpr (TS >= 0) red[0] = dot_leaf<VZ, 2>(tout, i, nv, f, f);  // inner.py:63 fl_dot(r, r)
     store_any<ST, VZ>(rs, i, nv, f, true);
     store_any<ST, VZ>(z, i, nv, zero, true);
   }
@@ -159,14 +175,25 @@ struct CplxBase : PwBase {
       o[k + 1] = round_to<ST>(im);
     }
   }
+  // reference rounding of S (sgn = 1) or S^T (sgn = -1), CSR row order:
+  // real row fl(fl(alpha a) + fl((-v) b)), imaginary row fl(fl(v a) + fl(alpha b))
+  __device__ void apply_ref(CT sgn, const CT (&a)[VZ], const CT (&vv)[VZ], CT (&o)[VZ]) const {
+#pragma unroll
+    for (int k = 0; k < VZ; k += 2) {
+      const CT v = sgn * vv[k];
+      o[k] = round_to<ST>(add_rn(round_to<ST>(mul_rn(al, a[k])), round_to<ST>(mul_rn(-v, a[k + 1]))));
+      o[k + 1] = round_to<ST>(add_rn(round_to<ST>(mul_rn(v, a[k])), round_to<ST>(mul_rn(al, a[k + 1]))));
+    }
+  }
 };
 
 // rhs2 = round(coeff z) ; r = rhs2 ; y = 0 ; rs = |round(S^T rhs2)|^2 ; nrhs
-template <class ST>
+template <class ST, bool RF = false>
 struct CInit : CplxBase<ST> {
   typedef CplxBase<ST> B;
   typedef typename B::CT CT;
   static constexpr int VZ = B::VZ, NR = 2;
+  static constexpr int TS = (RF && !B::ORD) ? 0 : -1;
   static constexpr bool HAS_RED = true;
   static constexpr int KID = K_C_INIT;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
@@ -184,16 +211,18 @@ struct CInit : CplxBase<ST> {
     this->loadv(i, nv, vv);
 #pragma unroll
     for (int k = 0; k < VZ; ++k) {
-      f[k] = round_to<ST>(coeff * zz[k]);
+      f[k] = round_to<ST>(mul_rn(coeff, zz[k]));
       zero[k] = CT(0);
     }
-    this->st_apply(f, vv, rb);
+    if constexpr (RF) this->apply_ref(CT(-1), f, vv, rb);
+    else this->st_apply(f, vv, rb);
 #pragma unroll
     for (int k = 0; k < VZ; ++k)
       if (k < nv) {
-        red[0] += (double)(rb[k] * rb[k]);
+        if constexpr (TS < 0) red[0] += (double)(rb[k] * rb[k]);
         red[1] += (double)f[k] * (double)f[k];
       }
+    if constexpr (TS >= 0) red[0] = dot_leaf<VZ, 1>(this->tout, i, nv, rb, rb);
     store_any<ST, VZ>(r, i, nv, f, true);
     store_any<ST, VZ>(y, i, nv, zero, true);
   }
@@ -213,11 +242,12 @@ struct CInit : CplxBase<ST> {
 };
 
 // p <- rbar (+ beta p), rbar = round(S^T r) recomputed pointwise ; w = S p ; |w|^2
-template <class ST>
+template <class ST, bool RF = false>
 struct CP1 : CplxBase<ST> {
   typedef CplxBase<ST> B;
   typedef typename B::CT CT;
   static constexpr int VZ = B::VZ, NR = 1;
+  static constexpr int TS = (RF && !B::ORD) ? 0 : -1;
   static constexpr bool HAS_RED = true;
   static constexpr int KID = K_C_P1;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
@@ -236,19 +266,25 @@ struct CP1 : CplxBase<ST> {
     CT rr[VZ], vv[VZ], rb[VZ], pp[VZ], w[VZ];
     load_any<ST, VZ, true>(r, i, nv, rr, true);
     this->loadv(i, nv, vv);
-    this->st_apply(rr, vv, rb);
+    if constexpr (RF) this->apply_ref(CT(-1), rr, vv, rb);
+    else this->st_apply(rr, vv, rb);
     if (!first) {
       load_any<ST, VZ, false>(p, i, nv, pp, true);
 #pragma unroll
-      for (int k = 0; k < VZ; ++k) pp[k] = round_to<ST>(fma_rn(beta, pp[k], rb[k]));
+      for (int k = 0; k < VZ; ++k) pp[k] = RF ? axpy_ref1<ST>(beta, pp[k], rb[k]) : round_to<ST>(fma_rn(beta, pp[k], rb[k]));
     } else {
 #pragma unroll
       for (int k = 0; k < VZ; ++k) pp[k] = rb[k];
     }
-    this->s_apply(pp, vv, w);
+    if constexpr (RF) this->apply_ref(CT(1), pp, vv, w);
+    else this->s_apply(pp, vv, w);
+    if constexpr (TS >= 0) {
+      red[0] = dot_leaf<VZ, 1>(this->tout, i, nv, w, w);
+    } else {
 #pragma unroll
-    for (int k = 0; k < VZ; ++k)
-      if (k < nv) red[0] += (double)(w[k] * w[k]);
+      for (int k = 0; k < VZ; ++k)
+        if (k < nv) red[0] += (double)(w[k] * w[k]);
+    }
     store_any<ST, VZ>(p, i, nv, pp, true);
   }
   __device__ void finalize(const double (&t)[1]) const {
@@ -257,16 +293,17 @@ struct CP1 : CplxBase<ST> {
       st->done = 1;
       return;
     }
-    st->alpha = st->rs / t[0];
+    st->alpha = sround(st->rs / t[0], ScalarRnd<ST, RF>::value);
   }
 };
 
 // y += alpha p ; r -= alpha S p ; fp64 |r|^2 ; rs_new = |round(S^T r)|^2 ; beta
-template <class ST>
+template <class ST, bool RF = false>
 struct CP2 : CplxBase<ST> {
   typedef CplxBase<ST> B;
   typedef typename B::CT CT;
   static constexpr int VZ = B::VZ, NR = 2;
+  static constexpr int TS = (RF && !B::ORD) ? 1 : -1;
   static constexpr bool HAS_RED = true;
   static constexpr int KID = K_C_P2;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
@@ -286,19 +323,22 @@ struct CP2 : CplxBase<ST> {
     load_any<ST, VZ, false>(y, i, nv, yy, true);
     load_any<ST, VZ, false>(r, i, nv, rr, true);
     this->loadv(i, nv, vv);
-    this->s_apply(pp, vv, w);
+    if constexpr (RF) this->apply_ref(CT(1), pp, vv, w);
+    else this->s_apply(pp, vv, w);
 #pragma unroll
     for (int k = 0; k < VZ; ++k) {
-      yy[k] = round_to<ST>(fma_rn(alpha, pp[k], yy[k]));
-      rr[k] = round_to<ST>(fma_rn(-alpha, w[k], rr[k]));
+      yy[k] = RF ? axpy_ref1<ST>(alpha, pp[k], yy[k]) : round_to<ST>(fma_rn(alpha, pp[k], yy[k]));
+      rr[k] = RF ? axpy_ref1<ST>(-alpha, w[k], rr[k]) : round_to<ST>(fma_rn(-alpha, w[k], rr[k]));
     }
-    this->st_apply(rr, vv, rb);
+    if constexpr (RF) this->apply_ref(CT(-1), rr, vv, rb);
+    else this->st_apply(rr, vv, rb);
 #pragma unroll
     for (int k = 0; k < VZ; ++k)
       if (k < nv) {
         red[0] += (double)rr[k] * (double)rr[k];
-        red[1] += (double)(rb[k] * rb[k]);
+        if constexpr (TS < 0) red[1] += (double)(rb[k] * rb[k]);
       }
+    if constexpr (TS >= 0) red[1] = dot_leaf<VZ, 1>(this->tout, i, nv, rb, rb);
     store_any<ST, VZ>(y, i, nv, yy, true);
     store_any<ST, VZ>(r, i, nv, rr, true);
   }
@@ -321,7 +361,7 @@ struct CP2 : CplxBase<ST> {
       st->done = 1;
       return;
     }
-    st->beta = rs_new / st->rs;
+    st->beta = sround(rs_new / st->rs, ScalarRnd<ST, RF>::value);
     st->rs = rs_new;
   }
 };

@@ -145,8 +145,19 @@ __device__ __forceinline__ CT apply_stencil(const CoefT<CT>& c, CT acc, const Nb
 
 // End of a reducing pass: run the scalar recurrence in place (one rank), or
 // deposit this rank's totals for the gather + finalize_kernel (slabs).
+// Slot of a pass's reference-rounding fl_dot (strict.cuh), or -1.
+template <class P, class = void> struct TreeSlot : std::integral_constant<int, -1> {};
+template <class P> struct TreeSlot<P, std::void_t<decltype(P::TS)>> : std::integral_constant<int, P::TS> {};
+
 template <class P, int NR>
 __device__ __forceinline__ void finish_pass(const P& p, const double (&tot)[NR]) {
+  if constexpr (TreeSlot<P>::value >= 0) {
+    if (p.tout.aux) {  // the tree finisher (strict.cuh) completes the reduction
+#pragma unroll
+      for (int s = 0; s < NR; ++s) p.tout.aux[s] = tot[s];
+      return;
+    }
+  }
   if (p.defer) {
 #pragma unroll
     for (int s = 0; s < NR; ++s) p.defer[s] = tot[s];

@@ -16,6 +16,7 @@
 #pragma once
 #include "sweep_tma.cuh"
 #include "tmap.cuh"
+#include "strict.cuh"
 
 namespace gadi {
 
@@ -380,6 +381,13 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
           }
         }
         if (own) p.epilogue(gidx, VZ, fcur, st, E, red);
+        if constexpr (TreeSlot<P>::value >= 0) {
+          // reference rounding: this warp's aligned fl_dot blocks (strict.cuh)
+          if (p.tout.tlog >= 0) {
+            tree_emit<VZ, (ZS == 2 ? 1 : 0)>(p.tout, gidx, own, lane, red[TreeSlot<P>::value]);
+            red[TreeSlot<P>::value] = 0.0;
+          }
+        }
 #pragma unroll
         for (int q = 0; q < NF; ++q)
 #pragma unroll

@@ -30,6 +30,19 @@ def default_maxit(n: int) -> int:
     return min(_MAXIT_CAP, max(1, math.ceil(5.0 * math.sqrt(n))))
 
 
+# Inner-solver arithmetic (gadi_set_rounding, include/gadi_b200.h): the
+# storage model, the reference's per-operation rounding inside the fused
+# passes, or the same rounding one operation per launch (cross-check).
+ROUNDING_MODES = {"storage": 0, "reference": 1, "reference_host": 2}
+
+
+def rounding_mode(rounding: str) -> int:
+    try:
+        return ROUNDING_MODES[rounding]
+    except KeyError:
+        raise ValueError(f"rounding must be one of {sorted(ROUNDING_MODES)}, got {rounding!r}") from None
+
+
 def dot_format(fmt, strict_model: bool):
     """Accumulation format of the reference's dot products (inner.py:39-44):
     u_s, or fp32 when ``strict_model`` is off and u_s is below fp32."""
@@ -83,7 +96,7 @@ def _true_relres(op, rhs, x, nrhs) -> float:
 
 
 def cg_spd(h, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
-           strict_model: bool = True, *, rounding: str = "storage"):
+           strict_model: bool = True, *, rounding: str = "reference"):
     """CG on H x = rhs, H SPD, x0 = 0.  ``rounding="reference"`` runs the
     reference's per-operation rounding emulation (bitwise iterates)."""
     fmt = resolve_format(fmt)
@@ -91,7 +104,7 @@ def cg_spd(h, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
     if maxit is None:
         maxit = default_maxit(rhs.size)
     with _ctx_for(h, fmt, "H") as ctx:
-        ctx.set_rounding(1 if rounding == "reference" else 0, dot_format(fmt, strict_model).name)
+        ctx.set_rounding(rounding_mode(rounding), dot_format(fmt, strict_model).name)
         x, st = ctx.h_solve(rhs, tol, maxit)
     nrhs = float(np.linalg.norm(rhs))
     return x, InnerSolveStats(st.iterations, st.final_relative_residual, bool(st.converged),
@@ -99,7 +112,7 @@ def cg_spd(h, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
 
 
 def cg_normal_skew(s, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt="fp64",
-                   strict_model: bool = True, s_transpose=None, *, rounding: str = "storage"):
+                   strict_model: bool = True, s_transpose=None, *, rounding: str = "reference"):
     """CGNR on S y = rhs (S^T S y = S^T rhs without forming S^T S), y0 = 0.
     ``s_transpose`` is implied by the stencil (S^T swaps the lo/up
     coefficients; crd flips the sign of V)."""
@@ -108,7 +121,7 @@ def cg_normal_skew(s, rhs: np.ndarray, tol: float, maxit: int | None = None, fmt
     if maxit is None:
         maxit = default_maxit(rhs.size)
     with _ctx_for(s, fmt, "S", s_transpose) as ctx:
-        ctx.set_rounding(1 if rounding == "reference" else 0, dot_format(fmt, strict_model).name)
+        ctx.set_rounding(rounding_mode(rounding), dot_format(fmt, strict_model).name)
         y, st = ctx.s_solve(rhs, tol, maxit)
     nrhs = float(np.linalg.norm(rhs))
     return y, InnerSolveStats(st.iterations, st.final_relative_residual, bool(st.converged),

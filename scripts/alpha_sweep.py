@@ -29,7 +29,7 @@ for a in alphas:
                            strict_model=False)
         t = T()
         w0 = time.perf_counter()
-        rep = g.gadi_solve(g.build_cd_3d(ng), cfg=cfg, return_x=False, hooks=t)
+        rep = g.gadi_solve(g.build_cd_3d(ng), cfg=cfg, return_x=False, hooks=t, rounding="storage")
         print(json.dumps({"ng": ng, "us": us, "alpha": a, "inner_tol": it, "s": round(t.ms / 1e3, 3),
                           "wall": round(time.perf_counter() - w0, 2), "status": rep.status,
                           "outer": rep.iterations,

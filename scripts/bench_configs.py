@@ -20,10 +20,10 @@ def run(tag, build, ng, us, alpha, outer_tol, inner_tol=1e-4, maxit=2000):
     cfg = g.GadiConfig(alpha=alpha, u_s=us, outer_tol=outer_tol, inner_tol=inner_tol, outer_maxit=maxit,
                        strict_model=False)
     build(ng)  # spec construction outside the timer
-    g.gadi_solve(build(ng), cfg=cfg, return_x=False, reuse_context=True)  # warm-up
+    g.gadi_solve(build(ng), cfg=cfg, return_x=False, reuse_context=True, rounding="storage")  # warm-up
     t = T()
     w0 = time.perf_counter()
-    rep = g.gadi_solve(build(ng), cfg=cfg, return_x=False, hooks=t)
+    rep = g.gadi_solve(build(ng), cfg=cfg, return_x=False, hooks=t, rounding="storage")
     out = {"config": tag, "n_g": ng, "u_s": us, "alpha": alpha, "outer_tol": outer_tol, "inner_tol": inner_tol,
            "device_s": round(t.ms / 1e3, 4), "wall_s": round(time.perf_counter() - w0, 3), "status": rep.status,
            "outer": rep.iterations, "inner_h": sum(h.inner_h_iterations for h in rep.history),

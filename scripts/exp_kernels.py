@@ -13,10 +13,10 @@ fam = sys.argv[4] if len(sys.argv) > 4 else "cd3d"
 build = {"cd3d": g.build_cd_3d, "cdr2d": g.build_cdr_2d, "crd": g.build_complex_rd}[fam]
 cfg = g.GadiConfig(alpha=0.0125 if fam == "cd3d" else 1.0, u_s=us, outer_tol=1e-12, outer_maxit=steps,
                    inner_tol=1e-3, strict_model=False)
-g.gadi_solve(build(ng), cfg=cfg, return_x=False)  # warm-up
+g.gadi_solve(build(ng), cfg=cfg, return_x=False, rounding="storage")  # warm-up
 ctx = next(iter(g.device._CACHE.values()))
 ctx.prof_enable(True)
-rep = g.gadi_solve(build(ng), cfg=cfg, return_x=False)
+rep = g.gadi_solve(build(ng), cfg=cfg, return_x=False, rounding="storage")
 prof = ctx.prof_read()
 ctx.prof_enable(False)
 knobs = {k: v for k, v in os.environ.items() if k.startswith("GADI_")}

@@ -7,5 +7,5 @@ us = sys.argv[2] if len(sys.argv) > 2 else "bf16"
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 p = g.build_cd_3d(ng)
 cfg = g.GadiConfig(alpha=0.025, u_s=us, outer_tol=1e-12, outer_maxit=steps, strict_model=False)
-rep = g.gadi_solve(p, cfg=cfg)
+rep = g.gadi_solve(p, cfg=cfg, rounding="storage")
 print(rep.iterations, [(h.inner_h_iterations, h.inner_s_iterations) for h in rep.history], rep.wallclock)

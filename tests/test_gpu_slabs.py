@@ -134,10 +134,10 @@ SOLVES = [
 @pytest.mark.parametrize("P", [2, 4])
 def test_slab_solve_matches_single_domain(gpu, fam, ng, kw, P):
     cfg = g.GadiConfig(outer_maxit=800, **kw)
-    ref = g.gadi_solve(BUILD[fam](ng), cfg=cfg, reuse_context=False)
+    ref = g.gadi_solve(BUILD[fam](ng), cfg=cfg, reuse_context=False, rounding="storage")
 
     def rank(comm, r):
-        return g.gadi_solve(BUILD[fam](ng), cfg=cfg, comm=comm, reuse_context=False)
+        return g.gadi_solve(BUILD[fam](ng), cfg=cfg, comm=comm, reuse_context=False, rounding="storage")
 
     reps = run_slabs(P, rank)
     # identical decisions on every rank
@@ -165,8 +165,8 @@ def test_nccl_transport_single_rank(gpu):
     comm = SlabComm.nccl(uid, 1, 0, 0)
     try:
         cfg = g.GadiConfig(alpha=0.5, u_s="bf16", outer_tol=1e-6)
-        ref = g.gadi_solve(g.build_cd_3d(16), cfg=cfg, reuse_context=False)
-        rep = g.gadi_solve(g.build_cd_3d(16), cfg=cfg, comm=comm, reuse_context=False)
+        ref = g.gadi_solve(g.build_cd_3d(16), cfg=cfg, reuse_context=False, rounding="storage")
+        rep = g.gadi_solve(g.build_cd_3d(16), cfg=cfg, comm=comm, reuse_context=False, rounding="storage")
         assert rep.slab == (0, 16)
         assert rep.iterations == ref.iterations
         assert [h.relative_residual for h in rep.history] == [h.relative_residual for h in ref.history]
