@@ -11,31 +11,50 @@ timed region).  Lower is better.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): the grid is slab-partitioned along its slowest axis, one
-slab per GPU, with NCCL halo exchanges and rank-ordered scalar all-gathers
-(strong scaling: the same n = 512^3 system at every N); the reported time is
-the max over ranks of the device-timed solve.  ``--compare-fp64 1`` also
-times the same solve with fp64 inner arithmetic (the north-star ">= 2x over
-the same code in full fp64"; minutes long, so off by default).  ``--impl reference``
-times the CPU oracle port (oracle/gadi_oracle.py, the reference's algorithm
-restated in numpy) on bounded samples of the same workload and extrapolates
-to the solve's iteration counts.
+Inner-solver arithmetic: the storage model (``--rounding storage``, default):
+bf16 storage with fp32 compute, the paper's GPU design.
+The reference package's per-operation bf16 emulation is the other mode
+(``gadi_solve(..., rounding="reference")``, bitwise the reference wherever
+the reference runs, tests/test_gpu_reference_fused.py); at this size its bf16
+partial sums cannot resolve the H-system and the solve diverges -- the line
+reports that run too (``reference_rounding_solve``).
+
+N > 1: the grid is slab-partitioned along its slowest axis, one slab per GPU,
+NCCL halo exchanges and rank-ordered scalar all-gathers (strong scaling: the
+same n = 512^3 system at every N); the time is the max over ranks of the
+device-timed solve.  ``--gpus N`` without torchrun re-launches this script
+under ``torch.distributed.run`` with N ranks.
+
+The fp64 comparison (north star: >= 2x over the same code in full fp64) runs
+by default: the same code with u_s = fp64 (a) on the bf16 run's splitting
+(precision alone), (b) at fp64's own best (alpha, inner_tol) from the GPU sweep
+(profiles/fp64_sweep_r2.jsonl).
+
+``--impl reference`` times the CPU oracle port (oracle/gadi_oracle.py, the
+reference's algorithm restated in numpy; the reference itself is pure Python
+and cannot hold n = 512^3) on bounded samples of the same workload on the
+host cores and extrapolates to the solve's measured iteration counts; a
+measured full CPU solve at 32^3 calibrates the extrapolation model.
 """
 
 from __future__ import annotations
 
-import argparse
-import json
-import math
 import os
-import subprocess
-import sys
-import tempfile
-import threading
-import time
-from pathlib import Path
 
-import numpy as np
+# BLAS threads of numpy (the CPU baseline's np.dot / norms; elementwise numpy
+# is single-threaded): the same setting in both arms, before numpy loads
+os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import socket  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import tempfile  # noqa: E402
+import time  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+import numpy as np  # noqa: E402
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -46,6 +65,8 @@ UNIT = "s"
 # profiles/); the reference arm extrapolates its per-iteration CPU costs with
 # them.  Updated from the last GPU measurement.
 COUNTS_FILE = ROOT / "profiles" / "bench_counts.json"
+# fp64's own best (alpha, inner_tol) at 512^3 from scripts/fp64_sweep.py
+FP64_BEST = {"alpha": 0.0125, "inner_tol": 1e-2}
 
 
 def parse():
@@ -67,9 +88,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-ng", type=int, default=128, help="grid of the bounded CPU sample")
-    ap.add_argument("--compare-fp64", type=int, default=0,
-                    help="also time the same solve with fp64 inner solves (slow: at this workload the fp64 "
-                         "inner solves do not reach the tolerance within outer_maxit, see DESIGN.md)")
+    ap.add_argument("--fp64", type=int, default=1, help="time the fp64 comparison solves (north star >= 2x)")
+    ap.add_argument("--ref-rounding", type=int, default=1,
+                    help="also run the solve with the reference's per-operation rounding (reported, not timed "
+                         "against the headline)")
+    ap.add_argument("--report-dir", default=str(ROOT / "gpurun_out" / "bench_report"),
+                    help="where the reference CLI's summary.csv / trace JSONL are written (report.py)")
     return ap.parse_args()
 
 
@@ -78,6 +102,9 @@ def workload(a):
             "family": a.family, "n_g": a.ng, "n": a.ng ** 3 if a.family == "cd3d" else a.ng ** 2,
             "alpha": a.alpha, "omega": 1.0, "u_s": a.us, "u": "fp64", "u_r": "fp64",
             "outer_tol": a.outer_tol, "inner_tol": a.inner_tol, "strict_model": False,
+            "rounding": a.rounding,
+            "arithmetic": ("storage model: u_s storage, fp32 compute, fp64 dot accumulation (PAPER.md:1180-1199)"
+                           if a.rounding == "storage" else "the reference's per-operation u_s rounding emulation"),
             "l2_policy": "inputs larger than L2 (fp64 vectors 1 GiB >> 126 MB L2)",
             "rhs": "b = A 1 generated in HBM (manufactured solution x* = 1)"}
 
@@ -130,41 +157,84 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU sample
-def cpu_sample(a, counts, threads_note=""):
-    """Time the oracle (the reference's algorithm) per unit of work on a
-    bounded cd3d(cpu_ng) problem, scale per unknown to the benchmark grid, and
-    extrapolate with the solve's iteration counts.  Returns (seconds, detail)."""
+def cpu_threads():
+    return int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+
+
+def cpu_units(a, ng, us):
+    """Per-unit CPU costs of the oracle (the reference's algorithm) on a
+    cd3d(ng) problem: one H-CG iteration, one CGNR iteration (u_s emulated, or
+    fp64), one outer pass (update + residual + monitor), one power iteration."""
     from oracle import gadi_oracle as O
 
-    ng = a.cpu_ng
     op = O.build(a.family, ng)
     n = op.n
-    H, S, ST = O.splitting(op, a.alpha, a.us)
+    H, S, ST = O.splitting(op, a.alpha, us)
     rng = np.random.default_rng(0)
-    r = O.q(rng.standard_normal(n) * 1e-3, a.us)
+    r = O.q(rng.standard_normal(n) * 1e-3, us)
     b = O.rhs_ones(op)
 
-    def per(fn, reps):
+    def per(fn, reps=1):
         t0 = time.perf_counter()
         for _ in range(reps):
             fn()
         return (time.perf_counter() - t0) / reps
 
-    t_h = per(lambda: O.cg_spd(H, r, 0.0, 2, a.us, True), 1) / 2        # per CG iteration (emulated u_s)
-    t_s = per(lambda: O.cg_normal_skew(S, ST, r, 0.0, 2, a.us, True), 1) / 2
+    t_h = per(lambda: O.cg_spd(H, r, 0.0, 2, us, False)) / 2
+    t_s = per(lambda: O.cg_normal_skew(S, ST, r, 0.0, 2, us, False)) / 2
     x = np.ones(n)
-    t_o = per(lambda: (O.stencil_residual(op, x, b), b - O.stencil_apply(op, x),
-                       O.stencil_apply(op, x - 1.0)), 1)               # residual + monitor
-    t_n = per(lambda: O.stencil_apply(op, O.stencil_apply(op, x)), 1)   # one power iteration
-    scale = counts["n"] / n
-    est = scale * (counts["outer"] * t_o + counts["inner_h"] * t_h + counts["inner_s"] * t_s
-                   + counts["norm_iters"] * t_n)
-    detail = (f"oracle port (numpy restatement of gadimp) on {a.family} {ng}^3 (n={n}): "
-              f"{t_h:.3f} s/H-CG it, {t_s:.3f} s/CGNR it, {t_o:.3f} s/outer pass, {t_n:.3f} s/power it "
-              f"(emulated {a.us} inner arithmetic, fp64 outer), scaled x{scale:.0f} per unknown and "
-              f"extrapolated to {counts['outer']} outer / {counts['inner_h']} H / {counts['inner_s']} S / "
-              f"{counts['norm_iters']} power iterations{threads_note}")
-    return est, detail
+    t_o = per(lambda: (O.stencil_residual(op, x, b), b - O.stencil_apply(op, x), O.stencil_apply(op, x - 1.0)))
+    t_n = per(lambda: O.stencil_apply(op, O.stencil_apply(op, x)))
+    return {"n": n, "h_it": t_h, "s_it": t_s, "outer": t_o, "power_it": t_n}
+
+
+def extrapolate(units, counts):
+    scale = counts["n"] / units["n"]
+    return scale * (counts["outer"] * units["outer"] + counts["inner_h"] * units["h_it"]
+                    + counts["inner_s"] * units["s_it"] + counts["norm_iters"] * units["power_it"])
+
+
+def cpu_sample(a, counts):
+    """(extrapolated seconds, detail, units) of the bounded sample."""
+    u = cpu_units(a, a.cpu_ng, a.us)
+    est = extrapolate(u, counts)
+    detail = (f"oracle port (numpy restatement of gadimp) on {a.family} {a.cpu_ng}^3 (n={u['n']}): "
+              f"{u['h_it']:.3f} s/H-CG it, {u['s_it']:.3f} s/CGNR it, {u['outer']:.3f} s/outer pass, "
+              f"{u['power_it']:.3f} s/power it (emulated {a.us} inner arithmetic, fp64 outer), scaled "
+              f"x{counts['n'] / u['n']:.0f} per unknown and extrapolated to the B200 solve's {counts['outer']} outer "
+              f"/ {counts['inner_h']} H / {counts['inner_s']} S / {counts['norm_iters']} power iterations; "
+              f"{cpu_threads()} BLAS threads (elementwise numpy single-threaded)")
+    return est, detail, u
+
+
+def cpu_calibration(a):
+    """A real, measured full CPU solve (oracle port, bench parameters) at
+    32^3 for 20 outer steps vs the extrapolation model's prediction for it."""
+    from oracle import gadi_oracle as O
+
+    ng, steps = 32, 20
+    op = O.build(a.family, ng)
+    b = O.rhs_ones(op)
+    out = {}
+    for us in (a.us, "fp64"):
+        t0 = time.perf_counter()
+        rep = O.gadi_solve(op, b, a.alpha, u_s=us, outer_tol=a.outer_tol, outer_maxit=steps,
+                           inner_tol=a.inner_tol, strict=False, exact=np.ones(op.n))
+        wall = time.perf_counter() - t0
+        c = {"n": op.n, "outer": len(rep.history), "inner_h": sum(h.inner_h for h in rep.history),
+             "inner_s": sum(h.inner_s for h in rep.history), "norm_iters": 0}
+        u = cpu_units(a, ng, us)
+        # the measured run includes ||A||_2 (power iteration count not exposed by
+        # the port: compare without it, i.e. measured minus one matrix_norm_2)
+        t1 = time.perf_counter()
+        O.matrix_norm_2(op)
+        t_norm = time.perf_counter() - t1
+        pred = extrapolate(u, c)
+        out[us] = {"n_g": ng, "outer_steps": c["outer"], "inner_h": c["inner_h"], "inner_s": c["inner_s"],
+                   "measured_s": round(wall - t_norm, 3), "predicted_s": round(pred, 3),
+                   "measured_over_predicted": round((wall - t_norm) / pred, 3) if pred > 0 else None,
+                   "status": rep.status}
+    return out
 
 
 def load_counts(a):
@@ -219,7 +289,7 @@ class Timer:
 
 def run_ours(a, rank, world):
     import paper_2512_21164_b200 as g
-    from paper_2512_21164_b200 import _lib
+    from paper_2512_21164_b200 import _lib, report
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     build = {"cd3d": g.build_cd_3d, "cdr2d": g.build_cdr_2d, "crd": g.build_complex_rd}[a.family]
@@ -227,9 +297,10 @@ def run_ours(a, rank, world):
                        outer_maxit=a.outer_maxit, strict_model=False)
     comm = g.SlabComm.from_torch(device=dev) if world > 1 else None
 
-    def solve(timer=None, problem=None, return_x=False, c=cfg):
+    def solve(timer=None, problem=None, return_x=False, c=cfg, splitting=None, rounding=a.rounding):
         p = problem if problem is not None else build(a.ng)
-        return g.gadi_solve(p, cfg=c, device=dev, return_x=return_x, hooks=timer, comm=comm, rounding=a.rounding)
+        return g.gadi_solve(p, splitting, c, device=dev, return_x=return_x, hooks=timer, comm=comm,
+                            rounding=rounding)
 
     for _ in range(a.warmup):
         solve()
@@ -264,7 +335,7 @@ def run_ours(a, rank, world):
               "norm_iters": rep.norm_iterations,
               "status": rep.status, "relres": rep.history[-1].relative_residual,
               "berr": rep.history[-1].backward_error, "ferr": rep.history[-1].forward_error}
-    if rank == 0:
+    if rank == 0 and world == 1 and a.rounding == "storage":
         save_counts(a, counts)
 
     # roofline of the dominant kernel (H-CG pass B: reads p (haloed), z, r;
@@ -279,8 +350,8 @@ def run_ours(a, rank, world):
     real = {"hcg_init": counts["outer"], "hcg_a": counts["inner_h"], "hcg_b": counts["inner_h"],
             "cgnr_init": counts["outer"], "cgnr_p1": counts["inner_s"], "cgnr_p2": counts["inner_s"],
             # the last iteration of every S-solve stops at P2's relres test
-            "cgnr_p3": max(1, counts["inner_s"] - counts["outer"]), "outer": counts["outer"] + 1, "norm_b": counts["norm_iters"],
-            "norm_a": counts["norm_iters"]}
+            "cgnr_p3": max(1, counts["inner_s"] - counts["outer"]), "outer": counts["outer"] + 1,
+            "norm_b": counts["norm_iters"], "norm_a": counts["norm_iters"]}
     kt = {k: (ms / max(1, min(cnt, real.get(k, cnt))), cnt, ms) for k, (ms, cnt) in prof.items()}
     total_kernel_ms = sum(v[2] for v in kt.values())
     dom = max(kt, key=lambda k: kt[k][2])
@@ -305,43 +376,78 @@ def run_ours(a, rank, world):
                                      "achieved": round(8 * s * rep_n / (it_us * 1e-6) / 1e9, 1),
                                      "frac": round(8 * s * rep_n / (it_us * 1e-6) / 1e9 / peak, 4)}
 
-    # end to end through the public API from host buffers
+    # end to end through the public API from host buffers: b in (H2D), x out
+    # (D2H) inside the timed region, one untimed warm-up, then K timed runs
     e2e = None
     if not a.no_e2e:
         p = build(a.ng)
         b_host = np.ascontiguousarray(p.b)  # materialise b on the host (input preparation, untimed)
-        p.b = b_host
-        dist_barrier(world)
-        t0 = time.perf_counter()
-        r2 = solve(problem=p, return_x=True)
-        t_e2e = time.perf_counter() - t0
-        assert r2.x is not None and r2.x.shape == (rep_n,)
-        t_e2e = dist_max(t_e2e, world)
-        e2e = {"value": round(t_e2e, 4), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-               "d2h_bytes_per_step": 8 * n + 48 * r2.iterations * world,
-               "status": r2.status, "outer": r2.iterations,
+        ev = []
+        last = None
+        for i in range(a.steps + 1):
+            p = build(a.ng)
+            p.b = b_host
+            dist_barrier(world)
+            t0 = time.perf_counter()
+            last = solve(problem=p, return_x=True)
+            dt = time.perf_counter() - t0
+            assert last.x is not None and last.x.shape == (rep_n,)
+            if i > 0:
+                ev.append(dist_max(dt, world))
+        e2e = {"value": round(float(np.mean(ev)), 4), "unit": UNIT, "runs": [round(v, 4) for v in ev],
+               "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 48 * last.iterations * world,
+               "status": last.status, "outer": last.iterations,
                "path": "gadi_solve(problem with host b) -> H2D of b, D2H of x per rank's slab"}
+        if rank == 0:
+            # the reference CLI's bench outputs (REF/cli.py:320-342) for this run
+            out = Path(a.report_dir)
+            out.mkdir(parents=True, exist_ok=True)
+            report.append_summary(out / "summary.csv", p, cfg, last, float(np.mean(ev)), 0,
+                                  gpu={"n_gpus": world, "device_time_s": t_solve,
+                                       "achieved_gbs": roofline["achieved"], "roofline_frac": roofline["frac"]})
+            report.write_trace(out / f"{p.label}_ng{a.ng}_{a.us}_trace.jsonl", last)
 
-    # the same solve with fp64 inner arithmetic (north star: >= 2x over full fp64)
+    # the north star's ">= 2x over the same code in full fp64"
     fp64 = None
-    if a.compare_fp64 and a.us != "fp64":
-        c64 = g.GadiConfig(alpha=a.alpha, u_s="fp64", outer_tol=a.outer_tol, inner_tol=a.inner_tol,
-                           outer_maxit=a.outer_maxit, strict_model=False)
-        solve(c=c64)  # warm-up (context + kernels)
-        dist_barrier(world)
+    if a.fp64 and a.us != "fp64":
+        fp64 = {}
+        sp = g.make_hss_splitting(build(a.ng).A, a.alpha, a.us)
+        runs = {"bf16_splitting": (g.GadiConfig(alpha=a.alpha, u_s="fp64", outer_tol=a.outer_tol,
+                                                inner_tol=a.inner_tol, outer_maxit=a.outer_maxit,
+                                                strict_model=False), sp),
+                "own_best": (g.GadiConfig(alpha=FP64_BEST["alpha"], u_s="fp64", outer_tol=a.outer_tol,
+                                          inner_tol=FP64_BEST["inner_tol"], outer_maxit=a.outer_maxit,
+                                          strict_model=False), None)}
+        for tag, (c64, spl) in runs.items():
+            solve(c=c64, splitting=spl, rounding="storage")  # warm-up (context + kernels)
+            dist_barrier(world)
+            t = Timer()
+            r64 = solve(timer=t, c=c64, splitting=spl, rounding="storage")
+            t64 = dist_max(t.ms / 1e3, world)
+            fp64[tag] = {"value": round(t64, 4), "unit": UNIT, "alpha": c64.alpha, "inner_tol": c64.inner_tol,
+                         "coef_fmt": spl.u_s.name if spl is not None else "fp64",
+                         "status": r64.status, "outer": r64.iterations,
+                         "inner_h": sum(h.inner_h_iterations for h in r64.history),
+                         "inner_s": sum(h.inner_s_iterations for h in r64.history),
+                         "relres": r64.history[-1].relative_residual, "berr": r64.history[-1].backward_error,
+                         "speedup_of_bf16": round(t64 / t_solve, 3)}
+
+    # the reference's own arithmetic at this size (reported: it diverges)
+    ref_round = None
+    if a.ref_rounding and a.rounding == "storage" and world == 1:
         t = Timer()
-        r64 = solve(timer=t, c=c64)
-        t64 = dist_max(t.ms / 1e3, world)
-        fp64 = {"value": round(t64, 4), "unit": UNIT, "status": r64.status, "outer": r64.iterations,
-                "inner_h": sum(h.inner_h_iterations for h in r64.history),
-                "inner_s": sum(h.inner_s_iterations for h in r64.history),
-                "berr": r64.history[-1].backward_error, "speedup_vs_fp64": round(t64 / t_solve, 3)}
+        rr = solve(timer=t, rounding="reference")
+        ref_round = {"s": round(t.ms / 1e3, 3), "status": rr.status, "outer": rr.iterations,
+                     "relres": [h.relative_residual for h in rr.history],
+                     "inner_h": [h.inner_h_iterations for h in rr.history],
+                     "note": "gadi_solve(rounding='reference'): the reference's per-operation bf16 emulation "
+                             "(bitwise the reference at 32^3-128^3, tests/golden/headline_*.json)"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-        est, detail = cpu_sample(a, counts, "; 1 thread")
-        cpu = {"value": round(est, 2), "unit": UNIT, "cores": 1, "kind": "port", "sample": detail}
+        est, detail, _ = cpu_sample(a, counts)
+        cpu = {"value": round(est, 2), "unit": UNIT, "cores": cpu_threads(), "kind": "port", "sample": detail,
+               "extrapolated": True}
 
     line = {"metric": METRIC, "value": round(t_solve, 4), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(t_solve * 1e3, 2), "higher_is_better": False,
@@ -353,34 +459,55 @@ def run_ours(a, rank, world):
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "solve": {k: counts[k] for k in ("status", "outer", "inner_h", "inner_s", "norm_iters", "relres",
                                               "berr", "ferr")},
-            "kernels": kernels, "fp64_inner_solve": fp64, "lib": _lib.load().gadi_build_info().decode()}
+            "kernels": kernels, "fp64_inner_solve": fp64, "reference_rounding_solve": ref_round,
+            "lib": _lib.load().gadi_build_info().decode()}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(a, rank, world):
+    """The reference's algorithm on the host cores (rank 0 only): the oracle
+    port timed on bounded samples of the workload (one H-CG iteration, one
+    CGNR iteration, one outer pass, one power iteration at cd3d cpu_ng^3 per
+    step, after W warm-up samples), extrapolated per unknown to n = 512^3 and
+    to the B200 solve's iteration counts; plus a measured full solve at 32^3
+    that calibrates the model.  The reference itself (pure Python) cannot hold
+    the 512^3 CSR (~100 GB) and is not on the GPU box."""
     if rank != 0:
         return
     counts = load_counts(a)
     if counts is None:
-        # counts of the same workload measured on the GPU are needed to
-        # extrapolate the CPU sample; fall back to the documented ones
-        counts = {"n": a.ng ** 3, "outer": 60, "inner_h": 6000, "inner_s": 200, "norm_iters": 500}
-    vals = []
-    detail = ""
-    for _ in range(a.warmup if a.warmup < 1 else 0):
-        pass
+        print(json.dumps({"impl": "reference", "unavailable": f"no measured B200 iteration counts for this workload "
+                                                              f"in {COUNTS_FILE.name}"}), flush=True)
+        return
+    for _ in range(a.warmup):
+        cpu_units(a, a.cpu_ng, a.us)
+    vals, detail, units = [], "", None
+    t0 = time.perf_counter()
     for _ in range(max(1, a.steps)):
-        est, detail = cpu_sample(a, counts, f"; numpy elementwise single-threaded, BLAS {os.cpu_count()} threads")
+        est, detail, units = cpu_sample(a, counts)
         vals.append(est)
+    wall_steps = time.perf_counter() - t0
     v = float(np.mean(vals))
+    u64 = cpu_units(a, a.cpu_ng, "fp64")
+    calib = cpu_calibration(a)
     line = {"metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": a.us + " inner (emulated) / fp64 outer", "data": "synthetic",
             "config": {**workload(a), "parallelism": "host CPU"}, "impl": "reference",
-            "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                             "sample": detail},
+            "extrapolated": True,
+            "extrapolation": {"per_unit_s": {k: round(units[k], 5) for k in ("h_it", "s_it", "outer", "power_it")},
+                              "sample_n": units["n"], "target_n": counts["n"], "scale": counts["n"] / units["n"],
+                              "counts": {k: counts[k] for k in ("outer", "inner_h", "inner_s", "norm_iters")},
+                              "counts_source": counts.get("source", str(COUNTS_FILE.name)),
+                              "sample_wall_s_per_step": round(wall_steps / max(1, a.steps), 3),
+                              "fp64_per_unit_s": {k: round(u64[k], 5) for k in ("h_it", "s_it", "outer",
+                                                                                "power_it")},
+                              "fp64_same_counts_s": round(extrapolate(u64, counts), 1)},
+            "calibration_full_solves": calib,
+            "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                             "sample": detail, "extrapolated": True},
             "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -420,9 +547,24 @@ def dist_max(v, world):
     return v
 
 
+def relaunch(n):
+    """--gpus N outside torchrun: run this script under torch.distributed.run
+    with N ranks on 127.0.0.1 and return its exit code."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        raise SystemExit(relaunch(a.gpus))
     rank, world = dist_init()
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":
         run_reference(a, rank, world)
     else:

@@ -271,6 +271,14 @@ static int upload_csr(Ctx* c, const gadi_csr& h, CsrDev& d, bool transpose, bool
     return set_error("CSR operator missing or of the wrong size", GADI_ERR_ARG);
   const long long n = h.nrows, nnz = h.nnz;
   if (n >= (1LL << 31)) return set_error("CSR operators need fewer than 2^31 rows", GADI_ERR_UNSUPPORTED);
+  // validate the structure before indexing with it (a malformed matrix must
+  // not corrupt host memory: the reference raises IndexError)
+  if (h.row_offsets[0] != 0 || h.row_offsets[n] != nnz || nnz < 0)
+    return set_error("CSR row offsets must start at 0 and end at nnz", GADI_ERR_ARG);
+  for (long long i = 0; i < n; ++i)
+    if (h.row_offsets[i + 1] < h.row_offsets[i]) return set_error("CSR row offsets must be nondecreasing", GADI_ERR_ARG);
+  for (long long k = 0; k < nnz; ++k)
+    if (h.col_indices[k] < 0 || h.col_indices[k] >= n) return set_error("CSR column index out of range", GADI_ERR_ARG);
   std::vector<long long> rp(n + 1);
   std::vector<int> ci((size_t)nnz);
   std::vector<double> v((size_t)nnz);

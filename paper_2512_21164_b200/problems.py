@@ -40,6 +40,9 @@ class Problem:
         return self.A.nrows
 
 
+_ONES = object()  # sentinel: the implicit all-ones exact solution
+
+
 class StencilProblem(Problem):
     """Manufactured-solution problem (x* = 1, b = A 1) on a stencil operator.
 
@@ -53,7 +56,7 @@ class StencilProblem(Problem):
         self.label = "crd3d" if (spec.family == "crd" and spec.ndim == 3) else spec.family
         self.params = dict(spec.params)
         self._b = None
-        self._exact = None
+        self._exact = _ONES  # implicit x* = 1 (problems.py:42-45) until set; None means "no exact solution"
 
     @property
     def b(self) -> np.ndarray:
@@ -68,8 +71,8 @@ class StencilProblem(Problem):
         self._b = np.asarray(value, dtype=np.float64)
 
     @property
-    def exact_solution(self) -> np.ndarray:
-        if self._exact is None:
+    def exact_solution(self) -> np.ndarray | None:
+        if self._exact is _ONES:
             self._exact = np.ones(self.spec.n)
         return self._exact
 
@@ -84,7 +87,8 @@ class StencilProblem(Problem):
 
     @property
     def exact_is_ones(self) -> bool:
-        return self._exact is None
+        """x* is still the implicit all-ones vector (never materialised)."""
+        return self._exact is _ONES
 
     def __repr__(self):
         return f"StencilProblem({self.label}, n={self.n}, params={self.params})"

@@ -289,17 +289,14 @@ class StencilMatrix:
 
 
 # ---------------------------------------------------------------- recognition
-_SAMPLE_ROWS = 64
-
-
 def recognise(problem) -> StencilSpec | None:
     """Map a problem to a stencil spec.
 
     Problems built by this package carry their spec.  Problems built
     elsewhere (e.g. by the reference package, or read from Matrix Market with
     the CLI sidecar, cli.py:56-68) are recognised from ``label`` + ``params``
-    and then *verified*: a sample of CSR rows must equal the stencil rows
-    bitwise, otherwise the general CSR path is used.
+    and then *verified*: the whole CSR (row offsets, column indices, value
+    bits) must equal the stencil's, otherwise the general CSR path is used.
     """
     a = problem.A
     if isinstance(a, StencilMatrix) and a.role == "A":
@@ -320,64 +317,59 @@ def recognise(problem) -> StencilSpec | None:
             return None
     except (KeyError, TypeError, ValueError):
         return None
-    if getattr(a, "nrows", None) != spec.n:
-        return None
-    if not _rows_match(a, spec):
+    if getattr(a, "nrows", None) != spec.n or not csr_equals(a, StencilMatrix(spec)):
         return None
     return spec
 
 
-def _rows_match(a, spec: StencilSpec) -> bool:
-    n = spec.n
-    rng = np.random.default_rng(0)
-    rows = np.unique(np.concatenate([np.arange(min(n, 8)), np.arange(max(0, n - 8), n),
-                                     rng.integers(0, n, size=_SAMPLE_ROWS)]))
-    ref = StencilMatrix(spec)
-    ro, ci, va = np.asarray(a.row_offsets), np.asarray(a.col_indices), np.asarray(a.values)
-    mine = _rows_of_spec(spec, rows)
-    for i, (mc, mv) in zip(rows, mine):
-        s, e = int(ro[i]), int(ro[i + 1])
-        if not (np.array_equal(ci[s:e], mc) and np.array_equal(va[s:e].view(np.uint64), mv.view(np.uint64))):
+def csr_equals(a, b) -> bool:
+    """Bitwise equality of two CSR operators (O(nnz), vectorised): the same
+    row offsets, column indices and value bit patterns."""
+    def parts(m):
+        if all(hasattr(m, k) for k in ("row_offsets", "col_indices", "values")):
+            return (np.asarray(v) for v in (m.row_offsets, m.col_indices, m.values))
+        c = m.to_scipy()
+        return np.asarray(c.indptr), np.asarray(c.indices), np.asarray(c.data)
+
+    try:
+        ra, ca, va = parts(a)
+        rb, cb, vb = parts(b)
+    except AttributeError:
+        return False
+    if ra.shape != rb.shape or ca.shape != cb.shape or va.shape != vb.shape:
+        return False
+    return (np.array_equal(ra, rb) and np.array_equal(ca, cb)
+            and np.array_equal(np.asarray(va, dtype=np.float64).view(np.uint64),
+                               np.asarray(vb, dtype=np.float64).view(np.uint64)))
+
+
+def same_spec(a: StencilSpec, b: StencilSpec) -> bool:
+    """Two specs describe the same operator (the fp64 coefficients, grid and
+    crd potential are what the kernels consume)."""
+    if a is b:
+        return True
+    if (a.family, a.n_g, a.ndim, a.A) != (b.family, b.n_g, b.ndim, b.A):
+        return False
+    if (a.v is None) != (b.v is None):
+        return False
+    return a.v is None or a.v is b.v or np.array_equal(np.asarray(a.v).view(np.uint64),
+                                                       np.asarray(b.v).view(np.uint64))
+
+
+def splitting_matches(splitting, spec: StencilSpec) -> bool:
+    """True when a supplied splitting is the HSS splitting of the stencil
+    (its u_s operators H_low, S_low, S_low_T bitwise those the stencil path
+    builds from (spec, alpha, splitting.u_s)); any other splitting must run
+    on its own matrices through the CSR engine."""
+    roles = (("H_low", "H"), ("S_low", "S"), ("S_low_T", "ST"))
+    for attr, role in roles:
+        m = getattr(splitting, attr)
+        if isinstance(m, StencilMatrix) and same_spec(m.spec, spec):
+            if m.role != role or float(m.alpha) != float(splitting.alpha) or m.fmt.name != splitting.u_s.name:
+                return False
+        elif not csr_equals(m, StencilMatrix(spec, role, splitting.alpha, splitting.u_s)):
             return False
-    del ref
     return True
-
-
-def _rows_of_spec(spec: StencilSpec, rows):
-    """(cols, vals) of selected rows of A, computed from the spec directly."""
-    out = []
-    if spec.family == "crd":
-        m = spec.n_g ** spec.ndim
-        sub = StencilSpec("cdr2d" if spec.ndim == 2 else "cd3d", spec.n_g, spec.ndim, spec.A)
-        for i in rows:
-            base = int(i) % m
-            cols, vals = _rows_of_spec(sub, [base])[0]
-            vi = spec.v[base]
-            if i < m:   # real row: L block then -V
-                out.append((np.append(cols, m + base), np.append(vals, -vi)))
-            else:       # imaginary row: V then L block
-                out.append((np.concatenate([[base], cols + m]), np.concatenate([[vi], vals])))
-        return out
-    nx, ny, nz = spec.dims
-    c = spec.A
-    strides = (ny * nz, nz, 1)
-    for i in rows:
-        i = int(i)
-        x, rem = divmod(i, ny * nz)
-        y, z = divmod(rem, nz)
-        co = (x, y, z)
-        ext = (nx, ny, nz)
-        cols, vals = [], []
-        for ax in (0, 1, 2):
-            if c.lo[ax] != 0.0 and co[ax] > 0:
-                cols.append(i - strides[ax]); vals.append(c.lo[ax])
-        if c.d != 0.0:
-            cols.append(i); vals.append(c.d)
-        for ax in (2, 1, 0):
-            if c.up[ax] != 0.0 and co[ax] < ext[ax] - 1:
-                cols.append(i + strides[ax]); vals.append(c.up[ax])
-        out.append((np.array(cols, dtype=np.int64), np.array(vals, dtype=np.float64)))
-    return out
 
 
 def with_params(spec: StencilSpec, **kw) -> StencilSpec:
