@@ -136,7 +136,20 @@ int gadi_comm_create_nccl(const unsigned char* id128, int nranks, int rank, int 
 /* In-process group of `nranks` slabs on one device, one host thread per rank
  * (single-GPU test harness of the decomposition); `key` names the group. */
 int gadi_comm_create_local(int key, int nranks, int rank, gadi_comm** out);
+/* As above; peer = 1: slab contexts built on it switch to the device-signalled
+ * peer transport (the same kernels as one process per GPU; see below). */
+int gadi_comm_create_local2(int key, int nranks, int rank, int peer, gadi_comm** out);
 int gadi_comm_destroy(gadi_comm* comm);
+/* Peer transport (csrc/peer.cu).  A slab context whose communicator asks for
+ * it (NCCL: unless GADI_COMM=nccl; local2: peer = 1) maps its neighbours'
+ * halo'd vectors, gather rows and epoch flags at creation (CUDA IPC handles
+ * exchanged over the base communicator; plain pointers within one process)
+ * and runs every halo exchange / scalar all-gather as kernels that write the
+ * peers' memory and synchronise on system-scope release/acquire flags -- no
+ * host in the loop, so the inner solves run as CUDA-graph WHILE loops.  If
+ * any rank cannot map its peers, every rank keeps the base transport.
+ * gadi_ctx_comm_kind reports the context's transport ("peer", "nccl", "local"). */
+const char* gadi_ctx_comm_kind(gadi_ctx* ctx);
 int gadi_comm_info(gadi_comm* comm, int* rank, int* nranks);
 int gadi_ctx_create_slab(const gadi_problem_desc* desc, int device, gadi_comm* comm, int64_t x0, int64_t x1,
                          gadi_ctx** out);

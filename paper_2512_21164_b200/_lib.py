@@ -102,6 +102,8 @@ SIGNATURES = {
     "gadi_comm_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "gadi_comm_create_nccl": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_VP)]),
     "gadi_comm_create_local": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(_VP)]),
+    "gadi_comm_create_local2": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_VP)]),
+    "gadi_ctx_comm_kind": (C.c_char_p, [_VP]),
     "gadi_comm_destroy": (C.c_int, [_VP]),
     "gadi_comm_info": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "gadi_ctx_create_slab": (C.c_int, [C.POINTER(ProblemDesc), C.c_int, _VP, C.c_int64, C.c_int64,
@@ -317,6 +319,9 @@ class Context:
         ms = C.c_double(0.0)
         check(self._L.gadi_timer_stop(self.h, C.byref(ms)))
         return float(ms.value)
+
+    def comm_kind(self) -> str:
+        return self._L.gadi_ctx_comm_kind(self.h).decode()
 
     def last_norm_ms(self) -> float:
         return float(self._L.gadi_last_norm_ms(self.h))

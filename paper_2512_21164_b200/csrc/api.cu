@@ -3,6 +3,7 @@
 // iteration, and the outer step that chains H-solve, S-solve and the fused
 // update/residual/monitor pass.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -176,6 +177,7 @@ static cudaError_t guarded_malloc(Ctx* c, void** p, size_t bytes, size_t esz) {
   if (e != cudaSuccess) return e;
   c->raws.push_back(raw);
   *p = raw + GUARD + mb;
+  c->gvec.push_back({*p, raw});
   // on the context stream: a legacy-stream cudaMemset is not ordered with the
   // (non-blocking) context stream and could land after the first upload
   return cudaMemsetAsync(raw, 0, bytes + 2 * (GUARD + mb), c->stream);
@@ -190,6 +192,10 @@ static int zero_vec(Ctx* c, void* p, size_t esz) {
 static void free_ctx(Ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->peer) {
+    c->comm = c->base_comm;
+    c->peer.reset();
+  }
   for (void* p : c->raws) cudaFree(p);
   c->raws.clear();
   for (CsrDev& m : c->csr) {
@@ -199,7 +205,7 @@ static void free_ctx(Ctx* c) {
     m = CsrDev();
   }
   void* sp[] = {c->v64, c->partials, c->VS, c->ticket, c->hst, c->sst, c->osum, c->nst, c->gbuf, c->wavecnt,
-                c->tree, c->tlvl, c->tticket, c->taux};
+                c->tree, c->tlvl, c->tticket, c->taux, c->pflags, c->pcnt};
   for (void* p : sp)
     if (p) cudaFree(p);
   void* hp[] = {c->h_hst, c->h_sst, c->h_osum, c->h_nst};
@@ -503,6 +509,12 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   }
   CHK(cudaStreamSynchronize(c->stream));
 #undef CHK
+  // slab contexts: device-signalled collectives over peer memory when every
+  // rank can map its neighbours (peer.cu); otherwise the base transport
+  if (c->comm && c->comm->want_peer && c->kind != GADI_CSR) {
+    if (peer_enable(c) != 0 && getenv("GADI_COMM_VERBOSE"))
+      fprintf(stderr, "gadi: peer transport off (%s), using %s\n", gadi_last_error(), c->comm->kind());
+  }
   *out = h;
   return 0;
 }
@@ -873,6 +885,7 @@ int gadi_set_rounding(gadi_ctx* h, int mode, int dot_fmt) {
 }
 
 double gadi_last_norm_ms(gadi_ctx* h) { return h->c.last_norm_ms; }
+const char* gadi_ctx_comm_kind(gadi_ctx* h) { return h->c.comm ? h->c.comm->kind() : "none"; }
 int64_t gadi_kernel_launches(gadi_ctx* h) { return h->c.launches; }
 
 }  // extern "C"

@@ -88,6 +88,18 @@ struct NcclComm : Comm {
     GADI_NCCL(g_nccl.GroupEnd());
     return 0;
   }
+  int exchange(const void* mine, size_t len, void* all, cudaStream_t s) override {
+    unsigned char* d = nullptr;
+    GADI_CUDA(cudaMalloc((void**)&d, len * (size_t)nranks));
+    GADI_CUDA(cudaMemcpyAsync(d + len * (size_t)rank, mine, len, cudaMemcpyHostToDevice, s));
+    const ncclResult_t r = g_nccl.AllGather(d + len * (size_t)rank, d, len, ncclUint8, comm, s);
+    cudaError_t e = cudaMemcpyAsync(all, d, len * (size_t)nranks, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(d);
+    if (r != ncclSuccess) return set_error(std::string("ncclAllGather: ") + g_nccl.GetErrorString(r), GADI_ERR_CUDA);
+    GADI_CUDA(e);
+    return 0;
+  }
   const char* kind() const override { return "nccl"; }
 };
 
@@ -103,6 +115,7 @@ struct Group {
   int arrived = 0;
   unsigned long long gen = 0;
   std::vector<void*> ptr;
+  std::vector<const void*> cptr;
   std::vector<long long> nx;
   int members = 0;
   void barrier() {
@@ -158,6 +171,13 @@ struct LocalComm : Comm {
     g->barrier();
     return 0;
   }
+  int exchange(const void* mine, size_t len, void* all, cudaStream_t) override {
+    g->cptr[rank] = mine;
+    g->barrier();
+    for (int j = 0; j < nranks; ++j) std::memcpy(static_cast<unsigned char*>(all) + len * (size_t)j, g->cptr[j], len);
+    g->barrier();
+    return 0;
+  }
   const char* kind() const override { return "local"; }
 };
 
@@ -187,6 +207,7 @@ int gadi_comm_create_nccl(const unsigned char* id, int nranks, int rank, int dev
   auto* c = new NcclComm();
   c->rank = rank;
   c->nranks = nranks;
+  c->want_peer = !(getenv("GADI_COMM") && std::string(getenv("GADI_COMM")) == "nccl");
   ncclResult_t r = g_nccl.CommInitRank(&c->comm, nranks, uid, rank);
   if (r != ncclSuccess) {
     delete c;
@@ -197,6 +218,10 @@ int gadi_comm_create_nccl(const unsigned char* id, int nranks, int rank, int dev
 }
 
 int gadi_comm_create_local(int key, int nranks, int rank, gadi_comm** out) {
+  return gadi_comm_create_local2(key, nranks, rank, 0, out);
+}
+
+int gadi_comm_create_local2(int key, int nranks, int rank, int peer, gadi_comm** out) {
   if (!out || nranks < 1 || rank < 0 || rank >= nranks) return set_error("bad communicator arguments", GADI_ERR_ARG);
   std::shared_ptr<Group> g;
   {
@@ -206,6 +231,7 @@ int gadi_comm_create_local(int key, int nranks, int rank, gadi_comm** out) {
       slot = std::make_shared<Group>();
       slot->n = nranks;
       slot->ptr.assign(nranks, nullptr);
+      slot->cptr.assign(nranks, nullptr);
       slot->nx.assign(nranks, 0);
     }
     if (slot->n != nranks) return set_error("local group size mismatch", GADI_ERR_ARG);
@@ -217,6 +243,7 @@ int gadi_comm_create_local(int key, int nranks, int rank, gadi_comm** out) {
   c->key = key;
   c->rank = rank;
   c->nranks = nranks;
+  c->want_peer = peer ? 1 : 0;
   *out = new gadi_comm{c};
   return 0;
 }

@@ -27,9 +27,14 @@ constexpr int GROW = 8;  // doubles per rank row of the gather buffer
 
 struct Comm {
   int rank = 0, nranks = 1;
+  int want_peer = 0;  // contexts built on this communicator switch to the peer transport (peer.cu)
   virtual ~Comm() {}
   virtual int gather(double* buf, int nr, cudaStream_t s) = 0;
   virtual int halo(void* base, size_t plane_bytes, long long nx, cudaStream_t s) = 0;
+  // host bytes: every rank's `len` bytes, in rank order, into `all` (setup only)
+  virtual int exchange(const void* mine, size_t len, void* all, cudaStream_t s) = 0;
+  // collectives are kernels only (graph-capturable, no host in the loop)
+  virtual bool device_only() const { return false; }
   virtual const char* kind() const = 0;
 };
 

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <array>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 #include "../../include/gadi_b200.h"
@@ -64,6 +65,17 @@ struct Ctx {
   long long gn = 0;             // global unknowns
   double* gbuf = nullptr;       // gather buffer [nranks][GROW]
   std::vector<void*> raws;      // raw device allocations (vectors with guards/halos)
+  struct GVec {
+    void* base;
+    void* raw;
+  };
+  std::vector<GVec> gvec;       // the halo'd vectors, in allocation order (peer transport)
+  // peer transport (peer.cu): the device-signalled collectives replace the
+  // base communicator once every rank has mapped its neighbours' buffers
+  std::unique_ptr<Comm> peer;
+  Comm* base_comm = nullptr;
+  unsigned long long* pflags = nullptr;  // epoch flags written by the peers
+  unsigned long long* pcnt = nullptr;    // this rank's epoch counters
   int us = GADI_FP64, u = GADI_FP64, ur = GADI_FP64;
   size_t ssz = 8;  // bytes per u_s element
   int sms = 148;
@@ -267,6 +279,10 @@ inline void prof_collect(Ctx* c) {
   }
   c->evused = 0;
 }
+
+int peer_enable(Ctx* c);
+int peer_export(Ctx* c, void* out, size_t cap, size_t* len);
+int peer_import(Ctx* c, const void* blobs, size_t blob_len);
 
 int exact_alloc(Ctx* c);
 void exact_free(Ctx* c);

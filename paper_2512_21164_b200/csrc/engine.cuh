@@ -299,7 +299,9 @@ static __global__ void loop_cond_kernel(cudaGraphConditionalHandle h, const Inne
   cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
 
-inline bool use_graphs(const Ctx* c) { return c->graphs && !c->comm && !c->prof; }
+// graph loops need collectives without the host: a single domain, or slabs on
+// the peer transport (peer.cu)
+inline bool use_graphs(const Ctx* c) { return c->graphs && (!c->comm || c->comm->device_only()) && !c->prof; }
 
 // Build (once per context) the graph whose WHILE body is `body` (which
 // enqueues the kernels of two iterations on c->stream).

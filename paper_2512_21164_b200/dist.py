@@ -9,10 +9,17 @@ decisions and the outer loop runs redundantly on every rank with no extra
 broadcast.  The collectives live in the C library (csrc/comm.cu);
 ``torch.distributed`` is only the plumbing that broadcasts the NCCL unique id.
 
+On one node the slab contexts switch from NCCL to the peer transport
+(csrc/peer.cu): the neighbours' buffers are mapped with CUDA IPC and every
+halo exchange / scalar all-gather is a few kernels writing peer memory and
+synchronising on device flags, so the inner loops run as CUDA graphs with no
+host involvement (``GADI_COMM=nccl`` keeps NCCL).
+
 ``SlabComm.local`` builds the same decomposition inside one process: P slabs
-on one device, one host thread per rank, collectives by device copies.  It is
-the single-GPU test harness of the multi-GPU path (identical kernels and
-engine code, only the transport differs).
+on one device, one host thread per rank, collectives by device copies behind
+host barriers -- or, with ``peer=True``, by the peer-transport kernels (the
+multi-GPU code path, plain pointers instead of IPC mappings).  It is the
+single-GPU test harness of the multi-GPU path.
 """
 
 from __future__ import annotations
@@ -77,10 +84,14 @@ class SlabComm:
         self.rank, self.nranks = int(r.value), int(n.value)
 
     @classmethod
-    def local(cls, key: int, nranks: int, rank: int) -> "SlabComm":
+    def local(cls, key: int, nranks: int, rank: int, peer: bool = False) -> "SlabComm":
+        """P slabs as P threads on one device.  peer=True: the contexts use the
+        device-signalled peer transport (csrc/peer.cu) -- the kernels of the
+        multi-GPU path -- instead of host barriers and copies."""
         h = C.c_void_p()
-        _lib.check(_lib.load().gadi_comm_create_local(int(key), int(nranks), int(rank), C.byref(h)))
-        return cls(h, "local")
+        _lib.check(_lib.load().gadi_comm_create_local2(int(key), int(nranks), int(rank), 1 if peer else 0,
+                                                       C.byref(h)))
+        return cls(h, "local-peer" if peer else "local")
 
     @staticmethod
     def unique_id() -> bytes:
