@@ -190,14 +190,14 @@ struct CsrOuterX : PwBase {
   const double* x;
   const SU* y;
   double* xout;
-  double scale;
+  double scale, inv_scale;
   int u32;
   __device__ bool prepare() { return true; }
   __device__ void apply(long long i, int nv, double (&)[1]) const {
 #pragma unroll
     for (int k = 0; k < VZ; ++k)
       if (k < nv) {
-        const double t = add_rn(x[i + k], __ddiv_rn(cvt_in<double>(y[i + k]), scale));
+        const double t = add_rn(x[i + k], mul_rn(cvt_in<double>(y[i + k]), inv_scale));  // scale = 2^k
         xout[i + k] = u32 ? (double)__double2float_rn(t) : t;
       }
   }

@@ -443,6 +443,7 @@ struct Engine {
     ox.y = (const ST*)c->Y;
     ox.xout = c->x[c->xcur ^ 1];
     ox.scale = scale;
+    ox.inv_scale = 1.0 / scale;
     ox.u32 = (c->u != GADI_FP64 && c->u != GADI_FP64X2) ? 1 : 0;
     GADI_TRY(launch_pw(c, ox));
     CsrOuterR<UR, HAS_E> o;
@@ -666,6 +667,7 @@ struct Engine {
     o.A = c->A;
     o.A32 = c->A32;
     o.scale = scale;
+    o.inv_scale = 1.0 / scale;
     o.ones = c->ones;
     o.u32 = (c->u != GADI_FP64 && c->u != GADI_FP64X2) ? 1 : 0;
     GADI_TRY(launch_sweep(c, o));

@@ -746,7 +746,7 @@ struct Outer : G, PassBase {
   OuterSums* out;
   CoefT<double> A;    // fp64 coefficients
   CoefT<float> A32;   // fp32-quantised coefficients (UR == 1)
-  double scale;
+  double scale, inv_scale;  // inv_scale = 1 / scale (exact: scale is a power of two)
   int ones;           // exact solution is the all-ones vector
   int u32;            // working precision fp32
   struct Raw { double x[VZ], y[VZ], xs[VZ]; };
@@ -783,7 +783,9 @@ struct Outer : G, PassBase {
     a.xs = (HAS_E && !ones) ? xs[i] : 1.0;
   }
   __device__ double xnew(double xv, double yv) const {
-    const double t = add_rn(xv, __ddiv_rn(yv, scale));  // gadi.py:163 x + y/scale
+    // gadi.py:163 x + y/scale: scale is a power of two, so y/scale and y * (1/scale)
+    // are the same exactly rounded value (one DMUL instead of a division sequence)
+    const double t = add_rn(xv, mul_rn(yv, inv_scale));
     return u32 ? (double)__double2float_rn(t) : t;
   }
   __device__ void fill(double xn, double xsv, double (&f)[NF]) const {

@@ -15,3 +15,5 @@ for k in Outer norm_fused HcgA; do
   sz=$(stat -c %s gpurun_out/full_${tag}_$k.ncu-rep 2>/dev/null || echo 0)
   if [ "$sz" -gt 18000000 ]; then rm -f gpurun_out/full_${tag}_$k.ncu-rep; fi
 done
+timeout 900 python scripts/floor_512.py > gpurun_out/floor_${tag}.jsonl 2>&1
+timeout 1800 python scripts/bench_configs.py 1 2 3 > gpurun_out/configs_${tag}.jsonl 2>&1
