@@ -41,9 +41,15 @@ using TmParam = typename std::conditional<TM != 0, TmapSet, TmapNone>::type;
 // 262 -> 275-280 and CgnrP2 / CgnrInit / CgnrP3 slower too: for a single
 // haloed input the ten parallel row copies finish a stage sooner than its
 // two box loads (profiles/tiling_r01.md)
+// GADI_TM_SINGLE = 1: passes with ONE haloed input (HcgB, CgnrInit, CgnrP2,
+// CgnrP3) load it as tensor-map boxes too (2 box loads per stage instead of
+// TY + 2 row copies)
+#ifndef GADI_TM_SINGLE
+#define GADI_TM_SINGLE 0
+#endif
 template <class P>
 struct TmaTm {
-  static constexpr bool value = SweepShape<P>::BZ == 32 && SweepShape<P>::BY > 1 && P::NIN >= 2;
+  static constexpr bool value = SweepShape<P>::BZ == 32 && SweepShape<P>::BY > 1 && P::NIN >= (GADI_TM_SINGLE ? 1 : 2);
 };
 // GADI_TM_EPIBOX = 1: the other 3-D passes with epilogue inputs load those
 // as one box each (TM = 2).  Measured: HcgB 263 -> 271 us, CgnrP2 280 ->

@@ -75,6 +75,8 @@ if "3" in which:  # cd3d 256^3, fp32 inner, relres 1e-6, GPR-i
     run("cfg3_gpr", g.build_cd_3d, 256, "fp32", alpha, 1e-6, 1e-3, 2000, extra={"gpr": gpr})
     for a in (0.025, 0.05):
         run("cfg3", g.build_cd_3d, 256, "fp32", a, 1e-6, 1e-3, 2000)
-if "5" in which:  # crd 2-D n_g = 8192 (n = 1.34e8), precision sweep, relres 1e-6
+if "5" in which:  # crd 2-D n_g = 8192 (n = 1.34e8), precision sweep, relres 1e-6;
+    # alpha = 1, inner_tol 1e-2 from the GPU sweeps (profiles/crd_sweep_r2_*.jsonl: alpha = 10 -- the
+    # reference tests' value at n_g <= 32 -- leaves the CGNR at maxit every step and stalls near 2e-6)
     for us in ("bf16", "fp32", "fp64"):
-        run("cfg5", g.build_complex_rd, 8192, us, 10.0, 1e-6, 1e-4, 400)
+        run("cfg5", g.build_complex_rd, 8192, us, 1.0, 1e-6, 1e-2, 400)

@@ -17,3 +17,6 @@ for k in Outer norm_fused HcgA; do
 done
 timeout 900 python scripts/floor_512.py > gpurun_out/floor_${tag}.jsonl 2>&1
 timeout 1800 python scripts/bench_configs.py 1 2 3 > gpurun_out/configs_${tag}.jsonl 2>&1
+# tensor-map variants (single-input passes, barrier-free outer pass) vs the default build
+timeout 600 python scripts/exp_kernels.py 512 bf16 3 > gpurun_out/exp_default_${tag}.json 2>&1
+GADI_LIB=$PWD/paper_2512_21164_b200/variants/libgadi_b200_tm1.so timeout 600 python scripts/exp_kernels.py 512 bf16 3 > gpurun_out/exp_tm1_${tag}.json 2>&1
