@@ -44,6 +44,10 @@ import os
 # BLAS threads of numpy (the CPU baseline's np.dot / norms; elementwise numpy
 # is single-threaded): the same setting in both arms, before numpy loads
 os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+# slab ranks on the peer transport spin on device flags: load every kernel at
+# context creation (a lazily loaded kernel's first launch can wait for the
+# device while a collective kernel spins)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 import argparse  # noqa: E402
 import json  # noqa: E402

@@ -281,6 +281,7 @@ inline void prof_collect(Ctx* c) {
 }
 
 int peer_enable(Ctx* c);
+int peer_check(Ctx* c);
 int peer_export(Ctx* c, void* out, size_t cap, size_t* len);
 int peer_import(Ctx* c, const void* blobs, size_t blob_len);
 

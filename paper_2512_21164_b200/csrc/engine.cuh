@@ -261,7 +261,7 @@ inline int poll_state(Ctx* c, InnerState* dev, InnerState* host) {
   GADI_CUDA(cudaMemcpyAsync(host, dev, sizeof(InnerState), cudaMemcpyDeviceToHost, c->stream));
   GADI_CUDA(cudaStreamSynchronize(c->stream));
   prof_collect(c);
-  return 0;
+  return peer_check(c);
 }
 
 // Enqueue inner iterations in batches (the previous solve's count + 1 first,

@@ -47,11 +47,26 @@ __device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void wait_ge(const unsigned long long* p, unsigned long long e) {
-  while (ld_acq(p) < e) __nanosleep(64);
+// Bounded wait: a peer that never arrives (a crashed rank, a mismatched
+// collective sequence) must not hang the GPU forever.  After ~10 s the wait
+// records the fault in the context's error word (checked by the host at its
+// next synchronisation: gadi_last_error) and gives up.
+__device__ __forceinline__ void wait_ge(const unsigned long long* p, unsigned long long e, unsigned* err, int what,
+                                        int rank) {
+  const long long t0 = clock64();
+  while (ld_acq(p) < e) {
+    __nanosleep(128);
+    if (clock64() - t0 > 20000000000LL) {
+      if (err) atomicCAS(err, 0u, (unsigned)what);
+      printf("gadi peer: rank %d wait %d timed out (epoch %llu, flag %llu)\n", rank, what, e, ld_acq(p));
+      return;
+    }
+  }
 }
 
 struct HaloArgs {
+  int rank;
+  unsigned* err;               // the context's peer error word
   unsigned long long* cnt;     // this rank's epoch counters [0] halo, [1] gather
   unsigned long long* own;     // this rank's flags
   unsigned long long* lo_f;    // lower neighbour's flags (nullptr: none)
@@ -68,8 +83,8 @@ __global__ void peer_halo_ready(HaloArgs a) {
   const unsigned long long e = ++a.cnt[0];
   if (a.lo_f) st_rel(a.lo_f + F_HREADY_HI * FSTRIDE, e);  // lower may write my plane -1
   if (a.hi_f) st_rel(a.hi_f + F_HREADY_LO * FSTRIDE, e);  // upper may write my plane nx
-  if (a.lo_f) wait_ge(a.own + F_HREADY_LO * FSTRIDE, e);
-  if (a.hi_f) wait_ge(a.own + F_HREADY_HI * FSTRIDE, e);
+  if (a.lo_f) wait_ge(a.own + F_HREADY_LO * FSTRIDE, e, a.err, 1, a.rank);
+  if (a.hi_f) wait_ge(a.own + F_HREADY_HI * FSTRIDE, e, a.err, 2, a.rank);
 }
 
 __global__ void peer_halo_push(HaloArgs a) {
@@ -97,12 +112,13 @@ __global__ void peer_halo_done(HaloArgs a) {
   __threadfence_system();
   if (a.lo_f) st_rel(a.lo_f + F_HDATA_HI * FSTRIDE, e);  // your upper halo is written
   if (a.hi_f) st_rel(a.hi_f + F_HDATA_LO * FSTRIDE, e);  // your lower halo is written
-  if (a.lo_f) wait_ge(a.own + F_HDATA_LO * FSTRIDE, e);
-  if (a.hi_f) wait_ge(a.own + F_HDATA_HI * FSTRIDE, e);
+  if (a.lo_f) wait_ge(a.own + F_HDATA_LO * FSTRIDE, e, a.err, 3, a.rank);
+  if (a.hi_f) wait_ge(a.own + F_HDATA_HI * FSTRIDE, e, a.err, 4, a.rank);
 }
 
 constexpr int MAXR = 64;
 struct GatherArgs {
+  unsigned* err;
   unsigned long long* cnt;
   unsigned long long* own;
   unsigned long long* pf[MAXR];  // peers' flags
@@ -117,7 +133,7 @@ __global__ void peer_gather(GatherArgs a) {
   for (int j = 0; j < a.nranks; ++j)
     if (j != a.rank) st_rel(a.pf[j] + (F_GREADY + a.rank) * FSTRIDE, g);
   for (int j = 0; j < a.nranks; ++j)
-    if (j != a.rank) wait_ge(a.own + (F_GREADY + j) * FSTRIDE, g);
+    if (j != a.rank) wait_ge(a.own + (F_GREADY + j) * FSTRIDE, g, a.err, 5, a.rank);
   const double* mine = a.buf + (size_t)a.rank * GROW;
   for (int j = 0; j < a.nranks; ++j)
     if (j != a.rank)
@@ -126,7 +142,7 @@ __global__ void peer_gather(GatherArgs a) {
   for (int j = 0; j < a.nranks; ++j)
     if (j != a.rank) st_rel(a.pf[j] + (gd + a.rank) * FSTRIDE, g);
   for (int j = 0; j < a.nranks; ++j)
-    if (j != a.rank) wait_ge(a.own + (gd + j) * FSTRIDE, g);
+    if (j != a.rank) wait_ge(a.own + (gd + j) * FSTRIDE, g, a.err, 6, a.rank);
 }
 
 // ------------------------------------------------------------------ export / import
@@ -164,6 +180,7 @@ struct PeerComm : Comm {
   int gather(double* buf, int nr, cudaStream_t s) override {
     GatherArgs a;
     std::memset(&a, 0, sizeof(a));
+    a.err = reinterpret_cast<unsigned*>(cnt + 2);
     a.cnt = cnt;
     a.own = flags;
     for (int j = 0; j < nranks; ++j) {
@@ -184,6 +201,8 @@ struct PeerComm : Comm {
     HaloArgs a;
     std::memset(&a, 0, sizeof(a));
     unsigned char* b = static_cast<unsigned char*>(base);
+    a.rank = rank;
+    a.err = reinterpret_cast<unsigned*>(cnt + 2);
     a.cnt = cnt;
     a.own = flags;
     a.nbytes = (long long)pb;
@@ -332,11 +351,25 @@ int peer_export(Ctx* c, void* out, size_t cap, size_t* len) {
   if (!c->pflags) {
     const size_t fb = sizeof(unsigned long long) * FSTRIDE * (size_t)nflags(c->comm->nranks);
     GADI_CUDA(cudaMalloc((void**)&c->pflags, fb));
-    GADI_CUDA(cudaMalloc((void**)&c->pcnt, 2 * sizeof(unsigned long long)));
+    // pcnt: [0] halo epoch, [1] gather epoch, [2] error word (peer_check)
+    GADI_CUDA(cudaMalloc((void**)&c->pcnt, 3 * sizeof(unsigned long long)));
     GADI_CUDA(cudaMemset(c->pflags, 0, fb));
-    GADI_CUDA(cudaMemset(c->pcnt, 0, 2 * sizeof(unsigned long long)));
+    GADI_CUDA(cudaMemset(c->pcnt, 0, 3 * sizeof(unsigned long long)));
   }
   return export_blob(c, static_cast<PeerBlob*>(out));
 }
 
+}  // namespace gadi
+
+namespace gadi {
+// Host side of the bounded waits: after a synchronisation, report a peer
+// that never arrived as an error instead of returning wrong results.
+int peer_check(Ctx* c) {
+  if (!c->peer || !c->pcnt) return 0;
+  unsigned e = 0;
+  GADI_CUDA(cudaMemcpy(&e, c->pcnt + 2, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  if (e) return set_error("peer transport: a neighbour did not arrive within 10 s (wait " + std::to_string(e) + ")",
+                          GADI_ERR_CUDA);
+  return 0;
+}
 }  // namespace gadi

@@ -87,7 +87,11 @@ class SlabComm:
     def local(cls, key: int, nranks: int, rank: int, peer: bool = False) -> "SlabComm":
         """P slabs as P threads on one device.  peer=True: the contexts use the
         device-signalled peer transport (csrc/peer.cu) -- the kernels of the
-        multi-GPU path -- instead of host barriers and copies."""
+        multi-GPU path -- instead of host barriers and copies.  The P ranks'
+        streams then spin on each other's flags on one GPU, so each needs its
+        own hardware queue: set CUDA_DEVICE_MAX_CONNECTIONS >= P + 2 before
+        CUDA initialises (tests/conftest.py sets 32).  One process per GPU
+        has one stream per device and no such constraint."""
         h = C.c_void_p()
         _lib.check(_lib.load().gadi_comm_create_local2(int(key), int(nranks), int(rank), 1 if peer else 0,
                                                        C.byref(h)))

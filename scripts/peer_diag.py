@@ -2,6 +2,9 @@
 python scripts/peer_diag.py P NG [graphs 0|1] [peer 0|1]"""
 import json
 import os
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 import random
 import sys
 import threading
@@ -38,7 +41,7 @@ ts = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(P)]
 for t in ts:
     t.start()
 for t in ts:
-    t.join(240)
+    t.join(120)
 alive = sum(t.is_alive() for t in ts)
 print(json.dumps({"P": P, "ng": ng, "graphs": os.environ.get("GADI_GRAPHS", "1"), "peer": peer, "alive": alive,
                   "errs": errs, "t_slabs": round(time.perf_counter() - t0, 2), "t_ref": round(t_ref, 2),

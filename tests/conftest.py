@@ -9,9 +9,21 @@
 """
 
 import json
+import os
 import subprocess
 import sys
 from pathlib import Path
+
+# The peer-transport tests run P slab ranks as P threads (P streams) on ONE
+# GPU whose collectives spin on device flags: every rank's stream needs its
+# own hardware work queue, or a spinning kernel can sit in front of the
+# kernel it waits for (the default of 8 queues is shared with other
+# streams).  Must be set before the process creates its CUDA context.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# ... and no kernel may be loaded lazily while a peer kernel spins: the first
+# launch of a kernel under CUDA_MODULE_LOADING=LAZY (the CUDA 12 default)
+# can wait for the device, i.e. for the spinning kernel, i.e. for this rank.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 import numpy as np
 import pytest
