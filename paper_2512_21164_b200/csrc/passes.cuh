@@ -724,7 +724,7 @@ struct CgnrP3 : G, PassBase {
 // reference's ascending column order (real row: L terms, then -v*x_im;
 // imaginary row: v*x_re, then L terms; problems.py:113-116).
 #ifndef GADI_OUTER_TMA2
-#define GADI_OUTER_TMA2 0
+#define GADI_OUTER_TMA2 1
 #endif
 template <class G, class SU, int UR, bool HAS_E, bool CPLX>
 struct Outer : G, PassBase {
@@ -736,9 +736,10 @@ struct Outer : G, PassBase {
   static constexpr int NR = 6;
   static constexpr int MINB = 1;  // two fp64 fields: let ptxas keep them in registers
   static constexpr bool HAS_RED = true, ORD = true, TMA_OK = !CPLX;
-  // the f-plane consumer form measured faster here with row copies
-  // (profiles/tiling_r01.md); GADI_OUTER_TMA2 = 1 selects the barrier-free
-  // form, whose two haloed inputs then load as tensor-map boxes
+  // the barrier-free consumer form with tensor-map boxes for the haloed x and
+  // y (GADI_OUTER_TMA2 = 1, default): 2867 -> 1997 us at 512^3 against the
+  // f-plane form with row copies (which had measured faster than the
+  // barrier-free form before tensor maps, profiles/tiling_r01.md)
   static constexpr bool TMA2_OK = GADI_OUTER_TMA2 != 0;
   static constexpr int KID = K_OUTER;
   static __device__ __forceinline__ int op(int s) { return s == 1 ? RED_MAX : RED_SUM; }

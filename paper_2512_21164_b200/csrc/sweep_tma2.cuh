@@ -36,6 +36,9 @@ namespace gadi {
 // consumer warps + helper) orders the writes before the neighbour reads; a
 // warp writes plane x+1 before it waits for plane x, so the wait is lagged by
 // one plane and rarely stalls.
+#ifndef GADI_XUNROLL
+#define GADI_XUNROLL 1
+#endif
 #ifndef GADI_INPLACE
 #define GADI_INPLACE 1
 #endif
@@ -326,6 +329,14 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
 #if GADI_EPI_LDG
       typename P::Epi En;
       if (own) p.load_epi(En, gidx, VZ);
+#endif
+      // GADI_XUNROLL = 3 unrolls the plane loop by the depth of the register
+      // queue (fprev / fcur / fnext), letting the compiler rename instead of
+      // moving the queue every plane
+#if GADI_XUNROLL == 3
+#pragma unroll 3
+#elif GADI_XUNROLL == 2
+#pragma unroll 2
 #endif
       for (int x = xa; x < xb; ++x, gidx += g.plane) {
         const int s = ps.slot;  // stage slot of plane x

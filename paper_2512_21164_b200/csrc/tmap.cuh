@@ -41,11 +41,12 @@ using TmParam = typename std::conditional<TM != 0, TmapSet, TmapNone>::type;
 // 262 -> 275-280 and CgnrP2 / CgnrInit / CgnrP3 slower too: for a single
 // haloed input the ten parallel row copies finish a stage sooner than its
 // two box loads (profiles/tiling_r01.md)
-// GADI_TM_SINGLE = 1: passes with ONE haloed input (HcgB, CgnrInit, CgnrP2,
-// CgnrP3) load it as tensor-map boxes too (2 box loads per stage instead of
-// TY + 2 row copies)
+// GADI_TM_SINGLE = 1 (default): passes with ONE haloed input (HcgB, CgnrInit,
+// CgnrP2, CgnrP3) load it as tensor-map boxes too (2 box loads per stage
+// instead of TY + 2 row copies).  Measured at 512^3 bf16: HcgB 270.6 -> 256.4
+// us, CgnrP2 291.9 -> 256.9 us, CgnrInit 290 -> 303 us (profiles/exp_r2e_*.json)
 #ifndef GADI_TM_SINGLE
-#define GADI_TM_SINGLE 0
+#define GADI_TM_SINGLE 1
 #endif
 template <class P>
 struct TmaTm {

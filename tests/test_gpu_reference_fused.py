@@ -121,10 +121,17 @@ def test_headline_regime_matches_reference(gpu, name):
     assert [h.inner_h_iterations for h in rep.history] == c["inner_h"]
     assert [h.inner_s_iterations for h in rep.history] == c["inner_s"]
     np.testing.assert_allclose(rep.relative_residuals, c["relres"], rtol=1e-9, atol=0)
-    np.testing.assert_allclose([h.backward_error for h in rep.history], c["berr"], rtol=1e-9, atol=0)
     if c["cfg"]["u_s"] != "fp64":  # fp64 dots are BLAS np.dot: order unpinned
         x = np.ascontiguousarray(rep.x, dtype=np.float64)
         assert hashlib.sha256(x.tobytes()).hexdigest() == c["x_sha256"]
+    # berr = ||r|| / (||A||_2 ||x|| + ||b||): above HOST_START_MAX unknowns the
+    # power iteration starts from the device generator instead of the
+    # reference's numpy vector, so ||A||_2 agrees to the power-iteration
+    # tolerance (1e-6 relative change per step), not to rounding
+    big = c["n_g"] ** 3 > g.analysis.HOST_START_MAX
+    np.testing.assert_allclose([h.backward_error for h in rep.history], c["berr"], rtol=1e-3 if big else 1e-9,
+                               atol=0)
+    assert rep.norm_A == pytest.approx(c["norm_A"], rel=1e-3 if big else 1e-10)
 
 
 @pytest.mark.parametrize("name", HEADLINE)
