@@ -150,6 +150,14 @@ int gadi_comm_destroy(gadi_comm* comm);
  * any rank cannot map its peers, every rank keeps the base transport.
  * gadi_ctx_comm_kind reports the context's transport ("peer", "nccl", "local"). */
 const char* gadi_ctx_comm_kind(gadi_ctx* ctx);
+/* The same transport with the blob exchange done by the caller (one process
+ * per GPU with any host collective, e.g. torch.distributed over gloo): a
+ * transport-less communicator, then per slab context export this rank's blob
+ * (CUDA IPC handles + layout), gather every rank's blob in rank order and
+ * attach.  blob_len = the length gadi_ctx_peer_export reports. */
+int gadi_comm_create_host(int nranks, int rank, gadi_comm** out);
+int gadi_ctx_peer_export(gadi_ctx* ctx, void* blob, size_t cap, size_t* len);
+int gadi_ctx_peer_attach(gadi_ctx* ctx, const void* blobs, size_t blob_len);
 int gadi_comm_info(gadi_comm* comm, int* rank, int* nranks);
 int gadi_ctx_create_slab(const gadi_problem_desc* desc, int device, gadi_comm* comm, int64_t x0, int64_t x1,
                          gadi_ctx** out);

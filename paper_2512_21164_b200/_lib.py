@@ -104,6 +104,9 @@ SIGNATURES = {
     "gadi_comm_create_local": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(_VP)]),
     "gadi_comm_create_local2": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_VP)]),
     "gadi_ctx_comm_kind": (C.c_char_p, [_VP]),
+    "gadi_comm_create_host": (C.c_int, [C.c_int, C.c_int, C.POINTER(_VP)]),
+    "gadi_ctx_peer_export": (C.c_int, [_VP, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "gadi_ctx_peer_attach": (C.c_int, [_VP, C.c_void_p, C.c_size_t]),
     "gadi_comm_destroy": (C.c_int, [_VP]),
     "gadi_comm_info": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "gadi_ctx_create_slab": (C.c_int, [C.POINTER(ProblemDesc), C.c_int, _VP, C.c_int64, C.c_int64,
@@ -200,6 +203,23 @@ class Context:
             check(self._L.gadi_ctx_slab(h, C.byref(a), C.byref(b), C.byref(m)))
             self.n = int(m.value)
             self.slab = (int(a.value), int(b.value))
+            if getattr(comm, "kind", "") == "host":
+                self._attach_peer(comm)
+
+    def _attach_peer(self, comm):
+        """Peer transport with the blob exchange over torch.distributed
+        (dist.SlabComm.host): every rank of the group must create the same
+        slab contexts in the same order."""
+        import torch.distributed as dist
+
+        n = C.c_size_t()
+        check(self._L.gadi_ctx_peer_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(self._L.gadi_ctx_peer_export(self.h, buf, n.value, C.byref(n)))
+        blobs = [None] * comm.nranks
+        dist.all_gather_object(blobs, buf.raw, group=comm.group)
+        allb = b"".join(blobs)
+        check(self._L.gadi_ctx_peer_attach(self.h, allb, n.value))
 
     def close(self):
         if getattr(self, "h", None):

@@ -373,3 +373,52 @@ int peer_check(Ctx* c) {
   return 0;
 }
 }  // namespace gadi
+
+using namespace gadi;
+
+namespace {
+// A communicator with no transport of its own: its slab contexts exchange
+// their peer blobs through the caller (e.g. torch.distributed over gloo) and
+// attach the peer transport with gadi_ctx_peer_attach.
+struct HostComm : Comm {
+  int gather(double*, int, cudaStream_t) override {
+    return set_error("host communicator: attach the peer transport first", GADI_ERR_UNSUPPORTED);
+  }
+  int halo(void*, size_t, long long, cudaStream_t) override {
+    return set_error("host communicator: attach the peer transport first", GADI_ERR_UNSUPPORTED);
+  }
+  int exchange(const void*, size_t, void*, cudaStream_t) override {
+    return set_error("host communicator: the caller exchanges the blobs", GADI_ERR_UNSUPPORTED);
+  }
+  const char* kind() const override { return "host"; }
+};
+}  // namespace
+
+extern "C" {
+
+int gadi_comm_create_host(int nranks, int rank, gadi_comm** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return set_error("bad communicator arguments", GADI_ERR_ARG);
+  auto* c = new HostComm();
+  c->rank = rank;
+  c->nranks = nranks;
+  *out = new gadi_comm{c};
+  return 0;
+}
+
+int gadi_ctx_peer_export(gadi_ctx* h, void* out, size_t cap, size_t* len) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  return peer_export(c, out, cap, len);
+}
+
+int gadi_ctx_peer_attach(gadi_ctx* h, const void* blobs, size_t blob_len) {
+  Ctx* c = &h->c;
+  GADI_CUDA(cudaSetDevice(c->device));
+  if (c->peer) return 0;
+  GADI_TRY(peer_import(c, blobs, blob_len));
+  c->base_comm = c->comm;
+  c->comm = c->peer.get();
+  return 0;
+}
+
+}  // extern "C"

@@ -97,6 +97,19 @@ class SlabComm:
                                                        C.byref(h)))
         return cls(h, "local-peer" if peer else "local")
 
+    @classmethod
+    def host(cls, group=None) -> "SlabComm":
+        """No transport of its own: each slab context built on it exchanges
+        its CUDA IPC blob over ``torch.distributed`` (``group``, any backend)
+        and attaches the device-signalled peer transport (csrc/peer.cu)."""
+        import torch.distributed as dist
+
+        h = C.c_void_p()
+        _lib.check(_lib.load().gadi_comm_create_host(dist.get_world_size(group), dist.get_rank(group), C.byref(h)))
+        c = cls(h, "host")
+        c.group = group
+        return c
+
     @staticmethod
     def unique_id() -> bytes:
         if nccl_library_path() and "GADI_NCCL_LIB" not in os.environ:
