@@ -231,3 +231,31 @@ def test_peer_transport_eight_slabs_256(gpu, monkeypatch):
         assert [h.relative_residual for h in rep.history] == [h.relative_residual for h in reps[0].history]
     assert reps[0].status == ref.status == "Converged"
     assert abs(reps[0].iterations - ref.iterations) <= 1, (reps[0].iterations, ref.iterations)
+
+
+def test_peer_transport_two_processes_ipc(gpu):
+    """The multi-process path of the peer transport -- CUDA IPC handles
+    exported, exchanged over torch.distributed (gloo) and opened in another
+    process, system-scope flags across processes -- with two processes on
+    this one GPU (their kernels time-slice, so small grids only): the
+    2-slab solve matches the single domain."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, PYTHONPATH=str(root), CUDA_MODULE_LOADING="EAGER")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", f"--master-port={port}", str(root / "scripts" / "ipc_check.py"),
+                        "12"], env=env, capture_output=True, text=True, timeout=400)
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert r.returncode == 0 and len(lines) == 2, r.stdout[-2000:] + r.stderr[-2000:]
+    rank0 = next(x for x in lines if x["rank"] == 0)
+    assert rank0["ok"], rank0
+    assert lines[0]["outer"] == lines[1]["outer"]
