@@ -726,6 +726,9 @@ struct CgnrP3 : G, PassBase {
 #ifndef GADI_OUTER_TMA2
 #define GADI_OUTER_TMA2 1
 #endif
+#ifndef GADI_OUTER_MINB
+#define GADI_OUTER_MINB 2
+#endif
 template <class G, class SU, int UR, bool HAS_E, bool CPLX>
 struct Outer : G, PassBase {
   typedef double CT;
@@ -734,7 +737,10 @@ struct Outer : G, PassBase {
   static constexpr int NF = 1 + (HAS_E ? 1 : 0) + (UR != 0 ? 1 : 0);
   static constexpr int FU = NF - 1;
   static constexpr int NR = 6;
-  static constexpr int MINB = 1;  // two fp64 fields: let ptxas keep them in registers
+  // two fp64 fields: 134 registers at 1 CTA/SM; GADI_OUTER_MINB = 2
+  // (default) caps them at 102 for two CTAs per SM -- 64 bytes of spills,
+  // but 1982 -> 1510 us at 512^3 (profiles/exp_om2.json)
+  static constexpr int MINB = GADI_OUTER_MINB;
   static constexpr bool HAS_RED = true, ORD = true, TMA_OK = !CPLX;
   // the barrier-free consumer form with tensor-map boxes for the haloed x and
   // y (GADI_OUTER_TMA2 = 1, default): 2867 -> 1997 us at 512^3 against the
