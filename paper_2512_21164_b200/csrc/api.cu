@@ -322,6 +322,41 @@ static int upload_csr(Ctx* c, const gadi_csr& h, CsrDev& d, bool transpose, bool
   return 0;
 }
 
+// Optional L2 residency for one u_s vector of the inner solves
+// (GADI_L2_PERSIST_MB = persisting bytes, GADI_L2_VEC = R | Z | RB | P0):
+// an access-policy window on the context stream marks that share of the
+// vector's lines persisting, so the pass that writes it and the next pass
+// that reads it meet in L2 (kernel nodes captured from the stream inherit it).
+static void l2_persist_setup(Ctx* c) {
+  const char* e = getenv("GADI_L2_PERSIST_MB");
+  if (!e || atof(e) <= 0.0 || c->kind == GADI_CSR) return;
+  const char* which = getenv("GADI_L2_VEC") ? getenv("GADI_L2_VEC") : "R";
+  void* base = c->R;
+  if (!strcmp(which, "Z")) base = c->Z;
+  else if (!strcmp(which, "RB")) base = c->RB;
+  else if (!strcmp(which, "P0")) base = c->P[0];
+  int maxwin = 0, maxpers = 0;
+  cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+  cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+  const size_t want = (size_t)(atof(e) * 1048576.0);
+  const size_t limit = std::min(want, (size_t)maxpers);
+  const size_t bytes = c->ssz * (size_t)c->n;
+  const size_t win = std::min(bytes, (size_t)maxwin);
+  if (!limit || !win) return;
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit);
+  cudaStreamAttrValue a = {};
+  a.accessPolicyWindow.base_ptr = base;
+  a.accessPolicyWindow.num_bytes = win;
+  a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)limit / (double)win);
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+  if (getenv("GADI_L2_VERBOSE"))
+    fprintf(stderr, "gadi: L2 persist %s: window %zu B of %zu, persisting limit %zu B (max window %d, max persisting %d)\n",
+            which, win, bytes, limit, maxwin, maxpers);
+  cudaGetLastError();
+}
+
 static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm, int64_t x0, int64_t x1,
                       gadi_ctx** out) {
   if (!desc || !out) return set_error("null argument", GADI_ERR_ARG);
@@ -509,6 +544,7 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   }
   CHK(cudaStreamSynchronize(c->stream));
 #undef CHK
+  l2_persist_setup(c);
   // slab contexts: device-signalled collectives over peer memory when every
   // rank can map its neighbours (peer.cu); otherwise the base transport
   if (c->comm && c->comm->want_peer && c->kind != GADI_CSR) {
