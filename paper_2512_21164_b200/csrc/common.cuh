@@ -220,6 +220,37 @@ __device__ __forceinline__ void store_any(T* __restrict__ p, long long idx, int 
   }
 }
 
+// GADI_EXACT_PACK = 1 packs already-rounded bf16 values with PRMT instead of
+// F2FP: measured neutral to slightly worse (HcgB 257 -> 261 us,
+// profiles/ab_pack_zpad_r2.jsonl) -- off
+#ifndef GADI_EXACT_PACK
+#define GADI_EXACT_PACK 0
+#endif
+// Store VZ compute-type values that are already exact values of T (rounded
+// earlier in the pass): for bf16 the pair is packed by a byte permute of the
+// fp32 patterns' top halves (one PRMT on the integer pipe) instead of a
+// rounding conversion (F2FP); identical bits.  Other types as store_any.
+template <class T, int VZ, class CT>
+__device__ __forceinline__ void store_exact(T* __restrict__ p, long long idx, int nvalid, const CT (&v)[VZ], bool vec) {
+  if constexpr (GADI_EXACT_PACK && std::is_same<CT, float>::value && std::is_same<T, bf16>::value && VZ % 2 == 0) {
+    constexpr int BYTES = VZ * 2;
+    if (vec && nvalid >= VZ && BYTES % 16 == 0) {
+      unsigned w[VZ / 2];
+#pragma unroll
+      for (int j = 0; j < VZ; j += 2) {
+        unsigned d;
+        asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(d) : "r"(__float_as_uint(v[j])), "r"(__float_as_uint(v[j + 1])));
+        w[j / 2] = d;
+      }
+#pragma unroll
+      for (int c = 0; c < BYTES / 16; ++c)
+        reinterpret_cast<uint4*>(p + idx)[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+      return;
+    }
+  }
+  store_any<T, VZ>(p, idx, nvalid, v, vec);
+}
+
 // ------------------------------------------------------------ reductions
 enum RedOp { RED_SUM = 0, RED_MAX = 1 };
 

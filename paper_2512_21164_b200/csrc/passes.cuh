@@ -386,7 +386,7 @@ struct HcgA : G, PassBase {
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
-    store_any<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
+    store_exact<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
     if constexpr (TS >= 0) {
       red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, fc[0], s[0]);  // fl_dot(p, Hp, dfmt), inner.py:69
     } else {
@@ -454,8 +454,8 @@ struct HcgB : G, PassBase {
     axpy_m<ST, RF>(-alpha, hp, e.r, rn);     // inner.py:75
     if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rn, rn);  // inner.py:76
     else red[0] += dotv<CT, G::VZ>(rn, rn, nv);
-    store_any<ST, G::VZ>(z, i, nv, zn, g.vec);
-    store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
+    store_exact<ST, G::VZ>(z, i, nv, zn, g.vec);
+    store_exact<ST, G::VZ>(r, i, nv, rn, g.vec);
   }
   __device__ void finalize(const double (&t)[1]) const { fin_cg_beta(st, t[0], ScalarRnd<ST, RF>::value); }
 };
@@ -516,8 +516,8 @@ struct CgnrInit : G, PassBase {
       }
     }
     if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rb, rb);  // inner.py:116
-    store_any<ST, G::VZ>(r, i, nv, fc[0], g.vec);
-    store_any<ST, G::VZ>(rbar, i, nv, rb, g.vec);
+    store_exact<ST, G::VZ>(r, i, nv, fc[0], g.vec);
+    store_exact<ST, G::VZ>(rbar, i, nv, rb, g.vec);
     store_any<ST, G::VZ>(y, i, nv, zero, g.vec);
   }
   __device__ void finalize(const double (&t)[2]) const { fin_cgnr_init(st, t[0], t[1], tol, maxit); }
@@ -591,7 +591,7 @@ struct CgnrP1 : G, PassBase {
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
-    store_any<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
+    store_exact<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
     CT w[G::VZ];
     round_vec_m<ST, RF>(s[0], w);
     if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, w, w);  // inner.py:122
@@ -656,8 +656,8 @@ struct CgnrP2 : G, PassBase {
 #pragma unroll
     for (int k = 0; k < G::VZ; ++k)
       if (k < nv) red[0] += (double)rn[k] * (double)rn[k];
-    store_any<ST, G::VZ>(y, i, nv, yn, g.vec);
-    store_any<ST, G::VZ>(r, i, nv, rn, g.vec);
+    store_exact<ST, G::VZ>(y, i, nv, yn, g.vec);
+    store_exact<ST, G::VZ>(r, i, nv, rn, g.vec);
   }
   __device__ void finalize(const double (&t)[1]) const { fin_cgnr_relres(st, t[0]); }
 };
@@ -707,7 +707,7 @@ struct CgnrP3 : G, PassBase {
     }
     if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rb, rb);  // inner.py:135
     else red[0] += dotv<CT, G::VZ>(rb, rb, nv);
-    store_any<ST, G::VZ>(rbar, i, nv, rb, g.vec);
+    store_exact<ST, G::VZ>(rbar, i, nv, rb, g.vec);
   }
   __device__ void finalize(const double (&t)[1]) const { fin_cgnr_beta(st, t[0], ScalarRnd<ST, RF>::value); }
 };

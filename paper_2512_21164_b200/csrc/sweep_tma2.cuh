@@ -36,6 +36,11 @@ namespace gadi {
 // consumer warps + helper) orders the writes before the neighbour reads; a
 // warp writes plane x+1 before it waits for plane x, so the wait is lagged by
 // one plane and rarely stalls.
+// GADI_ZPAD_FIELDS (in-place passes): the helper warp also writes the fields
+// of the tile's two z-pad columns
+#ifndef GADI_ZPAD_FIELDS
+#define GADI_ZPAD_FIELDS 1
+#endif
 #ifndef GADI_XUNROLL
 #define GADI_XUNROLL 1
 #endif
@@ -88,6 +93,7 @@ __device__ void inplace_halo_rows(const P& p, const SweepGeom& g, unsigned char*
   using CT = typename P::CT;
   using ST = typename P::ST;
   constexpr int VZ = SweepShape<P>::VZ, TZ = SweepShape<P>::TZ, TY = SweepShape<P>::TY, NST = TS::NST;
+  constexpr int BZ_ = SweepShape<P>::BZ;
   SegIter it(g, gridDim.x, blockIdx.x);
   int tile, xa, xb;
   int gs = 0;
@@ -103,11 +109,36 @@ __device__ void inplace_halo_rows(const P& p, const SweepGeom& g, unsigned char*
       if (x >= xa && x < xb) {
         CT f[1][VZ];
         stage_fields<P, TS>(p, stages, slot, 0, lane * VZ, top_ok, f);
-        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, 0, lane)), lane * VZ,
+        store_exact<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, 0, lane)), lane * VZ,
                           VZ, f[0], true);
         stage_fields<P, TS>(p, stages, slot, TY + 1, lane * VZ, bot_ok, f);
-        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, TY + 1, lane)),
+        store_exact<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, TY + 1, lane)),
                           lane * VZ, VZ, f[0], true);
+#if GADI_ZPAD_FIELDS
+        // the z-neighbour fields just outside the tile (columns -1 and TZ) of
+        // every row, so the consumers' edge lanes load them instead of
+        // evaluating the field in a divergent branch
+        if (lane < 2 * (TY + 2)) {
+          const int r = lane >> 1, right = lane & 1;
+          const int tzl = right ? BZ_ - 1 : 0, zo = right ? TZ : -1;
+          const int zz = zt0 + zo, yy = y0 - 1 + r;
+          const bool ok = zz >= 0 && zz < g.nz && yy >= 0 && yy < g.ny;
+          CT fs[1];
+          if (ok) {
+            SmRow R;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) R.p[j] = nullptr;
+#pragma unroll
+            for (int j = 0; j < P::NIN; ++j) R.p[j] = stage_in_row<P, TS>(stages, slot, j, r, tzl);
+            typename P::RawS a;
+            p.load_raw_s_sm(a, R, zo);
+            p.field_s(a, fs);
+          } else {
+            fs[0] = CT(0);
+          }
+          reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, slot, P::FIELD_IN, r, tzl))[zo] = Store<ST>::from(fs[0]);
+        }
+#endif
         fence_proxy_async_smem();
       }
       __syncwarp();
@@ -289,7 +320,7 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
     auto put_field = [&](int st, const CT (&f)[NF][VZ]) {
       if constexpr (INPL) {
         using ST = typename P::ST;
-        store_any<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, st, P::FIELD_IN, ty + 1, tz)), tz * VZ, VZ,
+        store_exact<ST, VZ>(reinterpret_cast<ST*>(stage_in_row<P, TS>(stages, st, P::FIELD_IN, ty + 1, tz)), tz * VZ, VZ,
                           f[0], true);
         fence_proxy_async_smem();
         __syncwarp();
@@ -364,10 +395,19 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
         CT st[NF][VZ];
         // z-neighbours: shuffles inside a warp, the stage row at warp edges
         CT zl[ZS][NF], zr[ZS][NF];
+        if constexpr (INPL && GADI_ZPAD_FIELDS && ZS == 1 && NF == 1) {
+          // the helper warp wrote the tile's z-pad fields in place (columns
+          // -1 and TZ); interior warp edges read the neighbour lane's field row
+          using ST = typename P::ST;
+          const ST* row = reinterpret_cast<const ST*>(stage_in_row<P, TS>(stages, s, P::FIELD_IN, ty + 1, tz));
+          zl[0][0] = (lane == 0) ? cvt_in<CT>(row[tz * VZ - 1]) : CT(0);
+          zr[0][0] = (lane == 31) ? cvt_in<CT>(row[tz * VZ + VZ]) : CT(0);
+        } else {
 #pragma unroll
-        for (int j = 0; j < ZS; ++j) {
-          field_scalar(s, ty + 1, tz * VZ - ZS + j, lane == 0 && own && zb - ZS + j >= 0, zl[j]);
-          field_scalar(s, ty + 1, tz * VZ + VZ + j, lane == 31 && own && zb + VZ + j < g.nz, zr[j]);
+          for (int j = 0; j < ZS; ++j) {
+            field_scalar(s, ty + 1, tz * VZ - ZS + j, lane == 0 && own && zb - ZS + j >= 0, zl[j]);
+            field_scalar(s, ty + 1, tz * VZ + VZ + j, lane == 31 && own && zb + VZ + j < g.nz, zr[j]);
+          }
         }
 #pragma unroll
         for (int q = 0; q < NF; ++q) {
