@@ -112,6 +112,30 @@ static int norm_pass(Ctx* c, const double* in, double* out) {
   p.A = TRANS ? c->AT : c->A;
   return launch_sweep(c, p);
 }
+// the same pass followed by the halo exchange of its output (fused push on
+// the peer transport)
+template <int DIM, int ZS, bool CPLX, bool TRANS>
+static int norm_pass_halo(Ctx* c, const double* in, double* out) {
+  typedef GeoT<double, DIM, ZS> G;
+  NormPass<G, CPLX, TRANS> p;
+  p.ns = c->nst;
+  p.in = in;
+  p.outv = out;
+  p.v = c->v64;
+  p.A = TRANS ? c->AT : c->A;
+  HaloOut ho;
+  const bool hf = halo_begin(c, out, 8, ho);
+  GADI_TRY(launch_sweep(c, p, &ho));
+  return halo_end(c, out, 8, hf);
+}
+template <bool TRANS>
+static int norm_pass_h(Ctx* c, const double* in, double* out) {
+  if (c->kind == GADI_COMPLEX)
+    return c->ndim == 3 ? norm_pass_halo<3, 2, true, TRANS>(c, in, out)
+                        : norm_pass_halo<2, 2, true, TRANS>(c, in, out);
+  if (c->ndim == 3) return norm_pass_halo<3, 1, false, TRANS>(c, in, out);
+  return norm_pass_halo<2, 1, false, TRANS>(c, in, out);
+}
 
 template <bool TRANS>
 static int norm_pass_d(Ctx* c, const double* in, double* out) {
@@ -673,10 +697,15 @@ int gadi_norm2(gadi_ctx* h, const double* v0, uint64_t seed, double tol, int max
         std::swap(w, t);
         continue;
       }
-      GADI_TRY(norm_pass_d<false>(c, w, t));
-      GADI_TRY(halo(c, t, 8));
-      GADI_TRY(norm_pass_d<true>(c, t, w));
-      GADI_TRY(halo(c, w, 8));
+      if (c->comm && c->kind != GADI_CSR) {  // slabs: the passes push their halo planes
+        GADI_TRY(norm_pass_h<false>(c, w, t));
+        GADI_TRY(norm_pass_h<true>(c, t, w));
+      } else {
+        GADI_TRY(norm_pass_d<false>(c, w, t));
+        GADI_TRY(halo(c, t, 8));
+        GADI_TRY(norm_pass_d<true>(c, t, w));
+        GADI_TRY(halo(c, w, 8));
+      }
     }
     launched += nb;
     GADI_CUDA(cudaMemcpyAsync(c->h_nst, c->nst, sizeof(NormState), cudaMemcpyDeviceToHost, c->stream));

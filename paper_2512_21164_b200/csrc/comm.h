@@ -35,6 +35,14 @@ struct Comm {
   virtual int exchange(const void* mine, size_t len, void* all, cudaStream_t s) = 0;
   // collectives are kernels only (graph-capturable, no host in the loop)
   virtual bool device_only() const { return false; }
+  // Split-phase halo of a vector whose producing pass writes its own boundary
+  // planes straight into the neighbours' halo planes (peer transport):
+  // halo_begin before the pass (the neighbours' slots are free; returns the
+  // peer plane pointers for the pass, or false: use halo() after the pass),
+  // halo_end after it (the data has landed on both sides).
+  virtual bool halo_begin(void* /*base*/, size_t /*plane_bytes*/, long long /*nx*/, void** /*lo_plane*/,
+                          void** /*hi_plane*/, cudaStream_t) { return false; }
+  virtual int halo_end(void* /*base*/, cudaStream_t) { return 0; }
   virtual const char* kind() const = 0;
 };
 

@@ -141,9 +141,25 @@ inline long long tree_leaves(const Ctx* c, const TreeOut& t) {
   return (c->n + (1LL << t.tlog) - 1) >> t.tlog;
 }
 
+// Split-phase halo of the vector a pass produces (peer transport): before
+// the pass the neighbours' halo slots are claimed and their plane pointers
+// go into the pass (HaloOut); after it, halo_end publishes the data.  Other
+// transports: the ordinary halo exchange after the pass.
+inline bool halo_begin(Ctx* c, void* base, size_t esz, HaloOut& h) {
+  h = HaloOut{nullptr, nullptr};
+  if (!c->comm) return false;
+  return c->comm->halo_begin(base, esz * (size_t)c->ny * c->nz, c->nx, &h.lo, &h.hi, c->stream);
+}
+inline int halo_end(Ctx* c, void* base, size_t esz, bool fused) {
+  if (!c->comm) return 0;
+  if (fused) return c->comm->halo_end(base, c->stream);
+  return halo(c, base, esz);
+}
+
 template <class P>
-inline int launch_sweep(Ctx* c, P& p) {
+inline int launch_sweep(Ctx* c, P& p, const HaloOut* hout = nullptr) {
   using S = SweepShape<P>;
+  p.hout = hout ? *hout : HaloOut{nullptr, nullptr};
   p.partials = c->partials;
   p.ticket = c->ticket;
   p.defer = defer_row(c);
@@ -498,6 +514,8 @@ struct Engine {
     const CoefT<CT> H = cast_coef<CT>(c->H);
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
     auto iter = [&](int k) -> int {
+        HaloOut ho;
+        bool hf = false;
         if (k == 0) {
           HcgA<G, true, RF> a;
           a.st = c->hst;
@@ -505,7 +523,8 @@ struct Engine {
           a.pin = P[0];
           a.pout = P[1];
           a.H = H;
-          GADI_TRY(launch_sweep(c, a));
+          hf = halo_begin(c, P[1], sizeof(ST), ho);
+          GADI_TRY(launch_sweep(c, a, &ho));
         } else {
           HcgA<G, false, RF> a;
           a.st = c->hst;
@@ -513,17 +532,19 @@ struct Engine {
           a.pin = P[k & 1];
           a.pout = P[(k + 1) & 1];
           a.H = H;
-          GADI_TRY(launch_sweep(c, a));
+          hf = halo_begin(c, P[(k + 1) & 1], sizeof(ST), ho);
+          GADI_TRY(launch_sweep(c, a, &ho));
         }
-        GADI_TRY(halo(c, P[(k + 1) & 1], sizeof(ST)));
+        GADI_TRY(halo_end(c, P[(k + 1) & 1], sizeof(ST), hf));
         HcgB<G, RF> b;
         b.st = c->hst;
         b.p = P[(k + 1) & 1];
         b.z = (ST*)c->Z;
         b.r = (ST*)c->R;
         b.H = H;
-        GADI_TRY(launch_sweep(c, b));
-        return halo(c, c->R, sizeof(ST));
+        hf = halo_begin(c, c->R, sizeof(ST), ho);
+        GADI_TRY(launch_sweep(c, b, &ho));
+        return halo_end(c, c->R, sizeof(ST), hf);
     };
     if (use_graphs(c) && maxit > 1) {
       GADI_TRY(iter(0));
@@ -558,6 +579,8 @@ struct Engine {
     GADI_TRY(halo(c, c->RB, sizeof(ST)));
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
     auto iter = [&](int k) -> int {
+        HaloOut ho;
+        bool hf = false;
         if (k == 0) {
           CgnrP1<G, true, RF> p1;
           p1.st = c->sst;
@@ -565,7 +588,8 @@ struct Engine {
           p1.pin = P[0];
           p1.pout = P[1];
           p1.S = S;
-          GADI_TRY(launch_sweep(c, p1));
+          hf = halo_begin(c, P[1], sizeof(ST), ho);
+          GADI_TRY(launch_sweep(c, p1, &ho));
         } else {
           CgnrP1<G, false, RF> p1;
           p1.st = c->sst;
@@ -573,24 +597,27 @@ struct Engine {
           p1.pin = P[k & 1];
           p1.pout = P[(k + 1) & 1];
           p1.S = S;
-          GADI_TRY(launch_sweep(c, p1));
+          hf = halo_begin(c, P[(k + 1) & 1], sizeof(ST), ho);
+          GADI_TRY(launch_sweep(c, p1, &ho));
         }
-        GADI_TRY(halo(c, P[(k + 1) & 1], sizeof(ST)));
+        GADI_TRY(halo_end(c, P[(k + 1) & 1], sizeof(ST), hf));
         CgnrP2<G, RF> p2;
         p2.st = c->sst;
         p2.p = P[(k + 1) & 1];
         p2.y = (ST*)c->Y;
         p2.r = (ST*)c->R;
         p2.S = S;
-        GADI_TRY(launch_sweep(c, p2));
-        GADI_TRY(halo(c, c->R, sizeof(ST)));
+        hf = halo_begin(c, c->R, sizeof(ST), ho);
+        GADI_TRY(launch_sweep(c, p2, &ho));
+        GADI_TRY(halo_end(c, c->R, sizeof(ST), hf));
         CgnrP3<G, RF> p3;
         p3.st = c->sst;
         p3.r = (const ST*)c->R;
         p3.rbar = (ST*)c->RB;
         p3.ST_ = STc;
-        GADI_TRY(launch_sweep(c, p3));
-        return halo(c, c->RB, sizeof(ST));
+        hf = halo_begin(c, c->RB, sizeof(ST), ho);
+        GADI_TRY(launch_sweep(c, p3, &ho));
+        return halo_end(c, c->RB, sizeof(ST), hf);
     };
     if (use_graphs(c) && maxit > 1) {
       GADI_TRY(iter(0));
@@ -670,9 +697,11 @@ struct Engine {
     o.inv_scale = 1.0 / scale;
     o.ones = c->ones;
     o.u32 = (c->u != GADI_FP64 && c->u != GADI_FP64X2) ? 1 : 0;
-    GADI_TRY(launch_sweep(c, o));
+    HaloOut ho;
+    const bool hf = halo_begin(c, c->x[c->xcur ^ 1], sizeof(double), ho);
+    GADI_TRY(launch_sweep(c, o, &ho));
     c->xcur ^= 1;
-    return halo(c, c->x[c->xcur], sizeof(double));
+    return halo_end(c, c->x[c->xcur], sizeof(double), hf);
   }
 
   template <int DIM, int ZS, bool CPLX>

@@ -298,6 +298,34 @@ __device__ __forceinline__ void round_vec_m(const CT (&a)[VZ], CT (&o)[VZ]) {
   }
 }
 
+// Peer transport (peer.cu), fused halo push: the pass that produces a
+// stencil-input vector also stores its planes 0 and nx-1 straight into the
+// lower neighbour's plane nx_lo and the upper neighbour's plane -1 (NVLink
+// stores, fenced at system scope before halo_end's flags publish them),
+// instead of a separate copy kernel after the pass.
+struct HaloOut {
+  void* lo;  // element (y, z) of my plane 0 goes to lo + y nz + z (nullptr: none)
+  void* hi;  // element (y, z) of my plane nx-1 goes to hi + y nz + z
+};
+template <class ST, int VZ, class CT>
+__device__ __forceinline__ void store_out(const HaloOut& h, const SweepGeom& g, ST* out, long long i, int nv,
+                                          const CT (&v)[VZ]) {
+  store_exact<ST, VZ>(out, i, nv, v, g.vec);
+  if (h.lo || h.hi) {
+    const long long pl = i / g.plane, off = i - pl * g.plane;
+    bool sent = false;
+    if (h.lo && pl == 0) {
+      store_exact<ST, VZ>(static_cast<ST*>(h.lo), off, nv, v, g.vec);
+      sent = true;
+    }
+    if (h.hi && pl == g.nx - 1) {
+      store_exact<ST, VZ>(static_cast<ST*>(h.hi), off, nv, v, g.vec);
+      sent = true;
+    }
+    if (sent) __threadfence_system();
+  }
+}
+
 // Common plumbing every pass carries.
 struct PassBase {
   SweepGeom g;
@@ -312,6 +340,7 @@ struct PassBase {
   double* partials;
   unsigned int* ticket;
   TreeOut tout;   // reference rounding: fl_dot leaves (strict.cuh)
+  HaloOut hout;   // peer transport: the neighbours' halo planes of the output
 };
 
 // ============================================================== H-CG passes
@@ -386,7 +415,7 @@ struct HcgA : G, PassBase {
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
-    store_exact<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
+    store_out<ST, G::VZ>(hout, g, pout, i, nv, fc[0]);
     if constexpr (TS >= 0) {
       red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, fc[0], s[0]);  // fl_dot(p, Hp, dfmt), inner.py:69
     } else {
@@ -455,7 +484,7 @@ struct HcgB : G, PassBase {
     if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rn, rn);  // inner.py:76
     else red[0] += dotv<CT, G::VZ>(rn, rn, nv);
     store_exact<ST, G::VZ>(z, i, nv, zn, g.vec);
-    store_exact<ST, G::VZ>(r, i, nv, rn, g.vec);
+    store_out<ST, G::VZ>(hout, g, r, i, nv, rn);
   }
   __device__ void finalize(const double (&t)[1]) const { fin_cg_beta(st, t[0], ScalarRnd<ST, RF>::value); }
 };
@@ -591,7 +620,7 @@ struct CgnrP1 : G, PassBase {
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi&,
                            double (&red)[1]) const {
-    store_exact<ST, G::VZ>(pout, i, nv, fc[0], g.vec);
+    store_out<ST, G::VZ>(hout, g, pout, i, nv, fc[0]);
     CT w[G::VZ];
     round_vec_m<ST, RF>(s[0], w);
     if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, w, w);  // inner.py:122
@@ -657,7 +686,7 @@ struct CgnrP2 : G, PassBase {
     for (int k = 0; k < G::VZ; ++k)
       if (k < nv) red[0] += (double)rn[k] * (double)rn[k];
     store_exact<ST, G::VZ>(y, i, nv, yn, g.vec);
-    store_exact<ST, G::VZ>(r, i, nv, rn, g.vec);
+    store_out<ST, G::VZ>(hout, g, r, i, nv, rn);
   }
   __device__ void finalize(const double (&t)[1]) const { fin_cgnr_relres(st, t[0]); }
 };
@@ -707,7 +736,7 @@ struct CgnrP3 : G, PassBase {
     }
     if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rb, rb);  // inner.py:135
     else red[0] += dotv<CT, G::VZ>(rb, rb, nv);
-    store_exact<ST, G::VZ>(rbar, i, nv, rb, g.vec);
+    store_out<ST, G::VZ>(hout, g, rbar, i, nv, rb);
   }
   __device__ void finalize(const double (&t)[1]) const { fin_cgnr_beta(st, t[0], ScalarRnd<ST, RF>::value); }
 };
@@ -878,7 +907,7 @@ struct Outer : G, PassBase {
         }
       }
     }
-    store_any<double, VZ>(xout, i, nv, fc[0], g.vec);
+    store_out<double, VZ>(hout, g, xout, i, nv, fc[0]);
     store_any<double, VZ>(r, i, nv, rv, g.vec);
   }
   __device__ void finalize(const double (&t)[6]) const {
@@ -961,7 +990,7 @@ struct NormPass : G, PassBase {
       o[k] = s[0][k];
       if (TRANS && k < nv) red[0] += o[k] * o[k];
     }
-    store_any<double, VZ>(outv, i, nv, o, g.vec);
+    store_out<double, VZ>(hout, g, outv, i, nv, o);
   }
   __device__ void finalize(const double (&t)[1]) const { fin_norm(ns, t[0]); }
 };

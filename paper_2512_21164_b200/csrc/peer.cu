@@ -24,6 +24,7 @@
 // read the old halo / gather rows (no write-after-read hazard even when a
 // rank runs one collective ahead).
 #include <unistd.h>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -225,6 +226,48 @@ struct PeerComm : Comm {
     GADI_CUDA(cudaGetLastError());
     c->launches += 3;
     return 0;
+  }
+  bool halo_begin(void* base, size_t pb, long long nx, void** lo_plane, void** hi_plane, cudaStream_t s) override {
+    auto it = vmap.find(base);
+    if (it == vmap.end() || getenv_flag_off()) return false;
+    HaloArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.rank = rank;
+    a.err = reinterpret_cast<unsigned*>(cnt + 2);
+    a.cnt = cnt;
+    a.own = flags;
+    *lo_plane = *hi_plane = nullptr;
+    if (rank > 0) {
+      a.lo_f = pflags[rank - 1];
+      *lo_plane = it->second.lo + (size_t)nx_lo * pb;  // the lower neighbour's plane nx_lo
+    }
+    if (rank < nranks - 1) {
+      a.hi_f = pflags[rank + 1];
+      *hi_plane = it->second.hi - pb;  // the upper neighbour's plane -1
+    }
+    (void)nx;
+    peer_halo_ready<<<1, 1, 0, s>>>(a);
+    c->launches += 1;
+    return cudaGetLastError() == cudaSuccess;
+  }
+  int halo_end(void* base, cudaStream_t s) override {
+    HaloArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.rank = rank;
+    a.err = reinterpret_cast<unsigned*>(cnt + 2);
+    a.cnt = cnt;
+    a.own = flags;
+    if (rank > 0) a.lo_f = pflags[rank - 1];
+    if (rank < nranks - 1) a.hi_f = pflags[rank + 1];
+    (void)base;
+    peer_halo_done<<<1, 1, 0, s>>>(a);
+    c->launches += 1;
+    GADI_CUDA(cudaGetLastError());
+    return 0;
+  }
+  static bool getenv_flag_off() {
+    static const bool off = getenv("GADI_FUSED_HALO") && atoi(getenv("GADI_FUSED_HALO")) == 0;
+    return off;
   }
   int exchange(const void*, size_t, void*, cudaStream_t) override {
     return set_error("peer transport: exchange is a setup collective of the base communicator", GADI_ERR_UNSUPPORTED);
