@@ -41,6 +41,8 @@ int kernel_occupancy(const void* fn, int device, int nthreads, size_t smem, bool
   return 0;
 }
 
+static int getenv_int(const char* k) { return getenv(k) ? atoi(getenv(k)) : 0; }
+
 static size_t fmt_bytes(int f) {
   switch (f) {
     case GADI_BF16:
@@ -174,6 +176,12 @@ static int norm_fused_step(Ctx* c, const double* in, double* out) {
   p.outv = out;
   p.A = c->A;
   p.AT = c->AT;
+  // the v tile of a stage as one tensor-map box ((TZ + 2 HZ) x (TY + 2 HV)
+  // fp64, zero-filled outside the grid) instead of TY + 2 HV row copies
+  CUtensorMap tmw;
+  std::memset(&tmw, 0, sizeof(tmw));
+  p.use_tm = (DIM == 3 && c->tmap && !getenv_int("GADI_NORM_TM0") &&
+              tm_map(c, in, 8, S::TZ + 2 * S::HZ, S::VROWS, &tmw)) ? 1 : 0;
   int occ = 1;
   GADI_TRY(occupancy_of(c, norm_fused_kernel<DIM, DENSE>, S::NTOT, S::SMEM, &occ, true));
   p.g = make_geom(c, S::TZ, S::TY, S::VZ, (long long)occ * c->sms);
@@ -181,7 +189,7 @@ static int norm_fused_step(Ctx* c, const double* in, double* out) {
   const int nb = (int)std::min<long long>(units, (long long)occ * c->sms * c->waves);
   if (nb > c->pstride) return set_error("fused norm grid exceeds partials buffer", GADI_ERR_ARG);
   prof_begin(c, K_NORM_B);
-  norm_fused_kernel<DIM, DENSE><<<nb, S::NTOT, S::SMEM, c->stream>>>(p);
+  norm_fused_kernel<DIM, DENSE><<<nb, S::NTOT, S::SMEM, c->stream>>>(p, tmw);
   prof_end(c);
   c->launches++;
   GADI_CUDA(cudaGetLastError());

@@ -18,6 +18,7 @@
 // the two-pass form.
 #pragma once
 #include "sweep_tma.cuh"
+#include "tmap.cuh"
 
 namespace gadi {
 
@@ -45,7 +46,7 @@ struct NFShape {
   static constexpr int NH = DIM == 3 ? 2 : 1;
   static constexpr int NCONS = NT + 32 * NH;
   static constexpr int NTOT = NCONS + 32;
-  static constexpr int TBYTES = 3 * TPLANE * 8;
+  static constexpr int TBYTES = (3 * TPLANE * 8 + 127) / 128 * 128;  // stages 128-byte aligned (TMA boxes)
   static constexpr int BUDGET = 100 * 1024;
   static constexpr int NST_RAW = (BUDGET - TBYTES) / STAGE;
   static constexpr int NST = NST_RAW >= 8 ? 8 : 4;  // power of two: cheap stage indexing
@@ -63,6 +64,7 @@ struct NormFused {
   double* outv;      // w'
   CoefT<double> A, AT;
   double rnw;
+  int use_tm;  // the v tile of a stage is one tensor-map box (hardware zero fill), else row copies
   static constexpr int NR = 1;
   static constexpr bool HAS_RED = true;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
@@ -102,7 +104,8 @@ __device__ __forceinline__ double nf_stencil(const CoefT<double>& c, double xm, 
 }
 
 template <int DIM, bool DENSE>
-__global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2) norm_fused_kernel(NormFused<DIM, DENSE> p) {
+__global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
+    norm_fused_kernel(NormFused<DIM, DENSE> p, const __grid_constant__ CUtensorMap tmw) {
   using S = NFShape<DIM>;
   constexpr int VZ = S::VZ, BZ = S::BZ, TY = S::TY, TZ = S::TZ, HZ = S::HZ, HV = S::HV, HT = S::HT;
   constexpr int ROW = S::ROW, NST = S::NST, NT = S::NT, NCONS = S::NCONS, NWCONS = NCONS / 32;
@@ -139,6 +142,15 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2) norm_fused_kernel(NormF
         if (gs >= NST) mbar_wait(&empty[st], (unsigned)(((gs / NST) - 1) & 1));
         unsigned char* sb = stages + (size_t)st * S::STAGE;
         const bool pv = xp >= 0 && xp < g.nx;
+        if (p.use_tm) {
+          // one (TZ + 2 HZ) x (TY + 2 HV) box: rows / columns outside the grid arrive as zeros
+          if (lane == 0) {
+            mbar_expect_tx(&full[st], pv ? (unsigned)S::STAGE : 0u);
+            if (pv) tma_load_3d(sb, &tmw, zt0 - HZ, y0 - HV, xp, &full[st]);
+          }
+          __syncwarp();
+          continue;
+        }
         unsigned bytes = 0;
         if (pv)
           for (int r = 0; r < NCOPY; ++r) {
