@@ -770,7 +770,7 @@ struct Outer : G, PassBase {
   // (default) caps them at 102 for two CTAs per SM -- 64 bytes of spills,
   // but 1982 -> 1510 us at 512^3 (profiles/exp_om2.json)
   static constexpr int MINB = GADI_OUTER_MINB;
-  static constexpr bool HAS_RED = true, ORD = true, TMA_OK = !CPLX;
+  static constexpr bool HAS_RED = true, ORD = true, TMA_OK = true;  // crd: v via load_epi_v
   // the barrier-free consumer form with tensor-map boxes for the haloed x and
   // y (GADI_OUTER_TMA2 = 1, default): 2867 -> 1997 us at 512^3 against the
   // f-plane form with row copies (which had measured faster than the
@@ -841,10 +841,14 @@ struct Outer : G, PassBase {
   __device__ void field_s(const RawS& a, double (&f)[NF]) const { fill(xnew(a.x, a.y), a.xs, f); }
   __device__ void load_epi(Epi& e, long long i, int nv) const {
     load_any<double, VZ, true>(b, i, nv, e.b, g.vec);
+    load_epi_v(e, i, nv);
+  }
+  // crd: the potential of the lane's complex points (global, by complex index)
+  __device__ void load_epi_v(Epi& e, long long i, int nv) const {
     if constexpr (CPLX) {
 #pragma unroll
       for (int k = 0; k < VZ; k += 2) {
-        const double vv = (k < nv) ? v[(i + k) >> 1] : 0.0;
+        const double vv = (k < nv) ? __ldg(v + ((i + k) >> 1)) : 0.0;
         e.v[k] = vv;
         e.v[k + 1] = vv;
       }
@@ -924,7 +928,7 @@ template <class G, bool CPLX, bool TRANS>
 struct NormPass : G, PassBase {
   typedef double CT;
   static constexpr int NF = 1, NR = 1;
-  static constexpr bool HAS_RED = TRANS, ORD = true, TMA_OK = !CPLX;
+  static constexpr bool HAS_RED = TRANS, ORD = true, TMA_OK = true;  // crd: v via load_epi_v
   static constexpr int VZ = G::VZ;
   static constexpr int KID = TRANS ? K_NORM_B : K_NORM_A;
   static __device__ __forceinline__ int op(int) { return RED_SUM; }
@@ -959,11 +963,12 @@ struct NormPass : G, PassBase {
   __device__ void load_raw_s(RawS& a, long long i) const { a.a = in[i]; }
   __device__ void field(const Raw& a, int k, double (&f)[1]) const { f[0] = fv(a.a[k]); }
   __device__ void field_s(const RawS& a, double (&f)[1]) const { f[0] = fv(a.a); }
-  __device__ void load_epi(Epi& e, long long i, int nv) const {
+  __device__ void load_epi(Epi& e, long long i, int nv) const { load_epi_v(e, i, nv); }
+  __device__ void load_epi_v(Epi& e, long long i, int nv) const {
     if constexpr (CPLX) {
 #pragma unroll
       for (int k = 0; k < VZ; k += 2) {
-        const double vv = (k < nv) ? v[(i + k) >> 1] : 0.0;
+        const double vv = (k < nv) ? __ldg(v + ((i + k) >> 1)) : 0.0;
         e.v[k] = vv;
         e.v[k + 1] = vv;
       }

@@ -77,6 +77,12 @@ __device__ __forceinline__ CT apply_stencil(const CoefT<CT>& c, CT acc, CT xm, C
   return acc;
 }
 
+// Passes whose epilogue needs a per-point coefficient indexed differently
+// from the grid (the crd potential v, one per complex point) load it from
+// global memory in the TMA forms (load_epi_v), next to the staged inputs.
+template <class P, class = void> struct HasEpiV : std::false_type {};
+template <class P> struct HasEpiV<P, std::void_t<decltype(&P::load_epi_v)>> : std::true_type {};
+
 // Optional per-vector hooks: a pass may process a lane's whole VZ-vector at
 // once (packed fp32x2 arithmetic) instead of element by element.
 template <class P, class = void> struct HasStencilVec : std::false_type {};

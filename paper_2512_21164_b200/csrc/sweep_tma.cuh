@@ -537,6 +537,9 @@ __global__ void __launch_bounds__(TmaThreads<P>::NTOT, P::MINB) sweep_tma_kernel
         // 2. stencil(s) and epilogue of plane x
         typename P::Epi E;
         p.load_epi_sm(E, epi_row((int)(s % NST), ty), tz * VZ);
+        if constexpr (HasEpiV<P>::value) {
+          if (nvz == VZ) p.load_epi_v(E, gidx, VZ);
+        }
         CT st[NF][VZ];
 #pragma unroll
         for (int q = 0; q < NF; ++q) {

@@ -392,6 +392,9 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
 #else
         p.load_epi_sm(E, epi_row(s, ty), tz * VZ);
 #endif
+        if constexpr (HasEpiV<P>::value) {
+          if (own) p.load_epi_v(E, gidx, VZ);
+        }
         CT st[NF][VZ];
         // z-neighbours: shuffles inside a warp, the stage row at warp edges
         CT zl[ZS][NF], zr[ZS][NF];
