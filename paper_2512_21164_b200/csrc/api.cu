@@ -925,7 +925,16 @@ int gadi_set_rounding(gadi_ctx* h, int mode, int dot_fmt) {
                      GADI_ERR_ARG);
   if (dot_fmt < GADI_BF16 || dot_fmt > GADI_FP64) return set_error("bad dot format", GADI_ERR_ARG);
   GADI_CUDA(cudaSetDevice(c->device));
-  if (mode != 0 && c->comm) return set_error("reference rounding runs on a single domain", GADI_ERR_UNSUPPORTED);
+  if (mode == 2 && c->comm) return set_error("per-operation reference rounding runs on a single domain", GADI_ERR_UNSUPPORTED);
+  if (mode == 1 && c->comm && c->us != GADI_FP64) {
+    // the fl_dot trees of the slabs must be whole subtrees of the global tree:
+    // 2^k ranks, equal slabs of a power-of-two number of (complex) points
+    const int P = c->comm->nranks;
+    const long long pts = c->kind == GADI_COMPLEX ? c->n / 2 : c->n;
+    const bool pow2 = (P & (P - 1)) == 0 && (pts & (pts - 1)) == 0 && c->gnx % P == 0;
+    if (!pow2)
+      return set_error("reference rounding on slabs needs 2^k ranks and equal slabs of 2^m points", GADI_ERR_UNSUPPORTED);
+  }
   // the fused reference passes cover the stencil families; general CSR
   // operators (and u_s = fp64, whose per-operation emulation is not needed
   // for mode 2) keep the per-operation path

@@ -96,6 +96,9 @@ inline bool tma_aligned(const Ctx* c) {
 // run the pass's scalar recurrence on them (finalize_kernel).
 template <class P>
 inline int post_reduce(Ctx* c, const P& p) {
+  if constexpr (TreeSlot<P>::value >= 0) {
+    if (p.tout.tree) return 0;  // reference rounding: launch_tree gathers after its finisher
+  }
   if constexpr (P::HAS_RED) {
     if (c->comm) {
       GADI_TRY(c->comm->gather(c->gbuf, P::NR, c->stream));
@@ -119,10 +122,27 @@ inline int ilog2(long long v) {
 // its scalar recurrence (tree_finish_kernel, strict.cuh).
 template <class P>
 inline int launch_tree(Ctx* c, const P& p, long long leaves) {
-  const long long nb = std::max(1LL, (leaves + TF_BLK - 1) / TF_BLK);
-  prof_begin(c, K_TREE);
-  tree_finish_kernel<P><<<(int)nb, TF_NT, 0, c->stream>>>(p, leaves, c->tlvl, c->tticket);
-  prof_end(c);
+  auto finish = [&](const float* lv, long long m, int slot) -> int {
+    const long long nb = std::max(1LL, (m + TF_BLK - 1) / TF_BLK);
+    prof_begin(c, K_TREE);
+    tree_finish_kernel<P><<<(int)nb, TF_NT, 0, c->stream>>>(p, lv, m, c->tlvl, c->tticket, slot);
+    prof_end(c);
+    c->launches++;
+    GADI_CUDA(cudaGetLastError());
+    return 0;
+  };
+  if (!c->comm) return finish(c->tree, leaves, -1);
+  // slabs: this rank's subtree(s) into its gather row, then the tree across
+  // ranks (complex: the real and imaginary halves are separate subtrees)
+  const bool cplx = p.tout.cm > 0;
+  if (cplx) {
+    GADI_TRY(finish(c->tree, leaves / 2, P::TS));
+    GADI_TRY(finish(c->tree + leaves / 2, leaves / 2, P::NR));
+  } else {
+    GADI_TRY(finish(c->tree, leaves, P::TS));
+  }
+  GADI_TRY(c->comm->gather(c->gbuf, P::NR + 1, c->stream));
+  tree_combine_kernel<P><<<1, 1, 0, c->stream>>>(p, c->gbuf, c->comm->nranks, GROW, cplx ? 1 : 0);
   c->launches++;
   GADI_CUDA(cudaGetLastError());
   return 0;

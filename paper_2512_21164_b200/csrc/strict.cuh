@@ -330,14 +330,19 @@ __device__ __forceinline__ float block_tree(const float* __restrict__ src, long 
 // the per-block values, in further rounds of TF_BLK while more than one
 // remains) and run the pass's recurrence with the tree total in slot P::TS.
 // lvl holds >= 2 * ceil(m / TF_BLK) + 2 floats.
+// Slab decomposition (slot >= 0): the leaves are this rank's aligned subtree
+// of the global tree; the total goes into this rank's gather row (slot
+// `slot`; slot P::TS also carries the pass's fp64 totals) and
+// tree_combine_kernel finishes the tree across ranks.
 template <class P>
-__global__ void __launch_bounds__(TF_NT) tree_finish_kernel(P p, long long m, float* __restrict__ lvl,
-                                                            unsigned int* __restrict__ ticket) {
+__global__ void __launch_bounds__(TF_NT) tree_finish_kernel(P p, const float* __restrict__ leaves, long long m,
+                                                            float* __restrict__ lvl, unsigned int* __restrict__ ticket,
+                                                            int slot) {
   __shared__ bool last;
   if (!p.prepare()) return;
   const TreeOut& t = p.tout;
   const long long base = (long long)blockIdx.x * TF_BLK;
-  const float v = block_tree(t.tree + base, m - base, t.dk);
+  const float v = block_tree(leaves + base, m - base, t.dk);
   if (threadIdx.x == 0) {
     lvl[blockIdx.x] = v;
     __threadfence();
@@ -365,9 +370,48 @@ __global__ void __launch_bounds__(TF_NT) tree_finish_kernel(P p, long long m, fl
 #pragma unroll
     for (int s = 0; s < P::NR; ++s) tot[s] = t.aux ? t.aux[s] : 0.0;
     tot[P::TS] = (double)__ldcg(src);
-    p.finalize(tot);
+    if (slot < 0) {
+      p.finalize(tot);
+    } else {
+      if (slot == P::TS)
+#pragma unroll
+        for (int s = 0; s < P::NR; ++s) p.defer[s] = tot[s];
+      else
+        p.defer[slot] = tot[P::TS];
+    }
     *ticket = 0u;
   }
+}
+
+// Across ranks (P = 2^k equal aligned slabs): every rank's subtree total is a
+// node of the global fl_sum tree at the same level, in rank order, so the
+// rest of the tree is the pairwise tree over the gathered totals -- for a
+// complex vector over the real halves and the imaginary halves separately
+// (block order [re; im]), then one add.  The fp64 slots sum in rank order
+// as finalize_kernel does.  Every rank computes the same value.
+template <class P>
+__global__ void tree_combine_kernel(P p, const double* __restrict__ gbuf, int nranks, int row, int cplx) {
+  if (!p.prepare()) return;
+  const TreeOut& t = p.tout;
+  double tot[P::NR];
+#pragma unroll
+  for (int s = 0; s < P::NR; ++s) {
+    tot[s] = gbuf[s];
+    if (s != P::TS)
+      for (int r = 1; r < nranks; ++r) tot[s] = red_combine(P::op(s), tot[s], gbuf[(size_t)r * row + s]);
+  }
+  float a[64], b[64];
+  for (int r = 0; r < nranks; ++r) {
+    a[r] = (float)gbuf[(size_t)r * row + P::TS];
+    b[r] = cplx ? (float)gbuf[(size_t)r * row + P::NR] : 0.f;
+  }
+  for (int w = 1; w < nranks; w *= 2)
+    for (int r = 0; r + w < nranks; r += 2 * w) {
+      a[r] = dadd(a[r], a[r + w], t.dk);
+      if (cplx) b[r] = dadd(b[r], b[r + w], t.dk);
+    }
+  tot[P::TS] = (double)(cplx ? dadd(a[0], b[0], t.dk) : a[0]);
+  p.finalize(tot);
 }
 
 }  // namespace gadi

@@ -259,3 +259,44 @@ def test_peer_transport_two_processes_ipc(gpu):
     rank0 = next(x for x in lines if x["rank"] == 0)
     assert rank0["ok"], rank0
     assert lines[0]["outer"] == lines[1]["outer"]
+
+
+REF_SLABS = [
+    ("cd3d", 16, dict(alpha=0.5, u_s="bf16", outer_tol=1e-6, strict_model=False)),
+    ("cd3d", 16, dict(alpha=0.5, u_s="fp32", outer_tol=1e-6)),
+    ("cdr2d", 32, dict(alpha=1.0, u_s="bf16", outer_tol=1e-10)),
+    ("crd", 16, dict(alpha=10.0, u_s="bf16", outer_tol=1e-6, strict_model=False)),
+]
+
+
+@pytest.mark.parametrize("fam,ng,kw", REF_SLABS)
+@pytest.mark.parametrize("P,peer", [(2, False), (2, True), (4, True)])
+def test_reference_rounding_on_slabs_is_bitwise(gpu, fam, ng, kw, P, peer):
+    """The reference's arithmetic across a slab decomposition: every rank's
+    fl_dot leaves form a whole subtree of the global pairwise tree (2^k ranks,
+    equal slabs of 2^m points), the subtree totals are gathered and the tree
+    finished across ranks (tree_combine_kernel) -- so the slab solve is
+    bitwise the single-domain reference-rounding solve (hence the reference's)."""
+    cfg = g.GadiConfig(outer_maxit=800, **kw)
+    ref = g.gadi_solve(BUILD[fam](ng), cfg=cfg, reuse_context=False, rounding="reference")
+
+    def rank(comm, r):
+        return g.gadi_solve(BUILD[fam](ng), cfg=cfg, comm=comm, reuse_context=False, rounding="reference")
+
+    reps = run_slabs(P, rank, peer=peer)
+    rep = reps[0]
+    assert rep.iterations == ref.iterations
+    assert [h.inner_h_iterations for h in rep.history] == [h.inner_h_iterations for h in ref.history]
+    assert [h.inner_s_iterations for h in rep.history] == [h.inner_s_iterations for h in ref.history]
+    assert np.array_equal(join_rows([q.x for q in reps], fam), ref.x)
+
+
+def test_reference_rounding_on_unaligned_slabs_is_refused(gpu):
+    cfg = g.GadiConfig(alpha=0.5, u_s="bf16", outer_tol=1e-6)
+
+    def rank(comm, r):
+        with pytest.raises(RuntimeError, match="2\\^k ranks"):
+            g.gadi_solve(g.build_cd_3d(16), cfg=cfg, comm=comm, reuse_context=False, rounding="reference")
+        return True
+
+    assert run_slabs(3, rank) == [True, True, True]
