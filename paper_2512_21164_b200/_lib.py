@@ -14,7 +14,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(os.environ.get("GADI_LIB", Path(__file__).resolve().parent / "libgadi_b200.so"))
+LIB_PATH = Path(os.environ.get("GADI_LIB") or Path(__file__).resolve().parent / "libgadi_b200.so")
 CSRC = Path(__file__).resolve().parent / "csrc"
 
 GADI_OK, GADI_ERR_CUDA, GADI_ERR_ARG, GADI_ERR_OOM, GADI_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
@@ -318,7 +318,7 @@ class Context:
         check(self._L.gadi_set_rounding(self.h, int(mode), FMT_CODES[dot_fmt]))
 
     KERNELS = ["hcg_init", "hcg_a", "hcg_b", "cgnr_init", "cgnr_p1", "cgnr_p2", "cgnr_p3",
-               "crd_init", "crd_p1", "crd_p2", "outer", "norm_a", "norm_b", "apply", "dot_tree"]
+               "crd_init", "crd_p1", "crd_p2", "outer", "norm_a", "norm_b", "apply", "dot_tree", "hcg_z"]
 
     def prof_enable(self, on=True):
         check(self._L.gadi_prof_enable(self.h, 1 if on else 0))

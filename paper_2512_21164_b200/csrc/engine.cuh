@@ -92,6 +92,16 @@ inline bool tma_aligned(const Ctx* c) {
   return (c->nz % P::VZ) == 0;
 }
 
+// Z-lag H-CG (passes.cuh HcgA): compiled in, selected per process by the
+// environment (GADI_ZLAG=1) when the pass runs on the barrier-free TMA form.
+// Measured at 512^3 bf16 (profiles/ab_zlag_r2.jsonl): HcgA 204 -> 278 us,
+// HcgB 256 -> 190 us, one H-CG iteration 460 -> 468 us -- off by default.
+template <class P>
+inline bool zlag_ok(const Ctx* c) {
+  if (!c->zlag_on) return false;
+  return tma_aligned<P>(c) && c->tma2 != 0 && TmaForm2<P>::value;
+}
+
 // Slab decomposition: after a reducing pass, gather every rank's totals and
 // run the pass's scalar recurrence on them (finalize_kernel).
 template <class P>
@@ -191,6 +201,9 @@ inline int launch_sweep(Ctx* c, P& p, const HaloOut* hout = nullptr) {
     // evenly among them (SegIter).  Barrier-free consumers (sweep_tma2.cuh)
     // unless GADI_TMA2=0 selects the f-plane form (sweep_tma.cuh).
     const bool v2 = c->tma2 != 0 && TmaForm2<P>::value;
+    if constexpr (HasSide<P>::value) {
+      if (!v2) return set_error("z-lag pass off the barrier-free sweep form", GADI_ERR_ARG);
+    }
     // tensor-map producer for the 3-D barrier-free passes (tmap.cuh): mode 1
     // boxes for two haloed inputs, mode 2 boxes for the epilogue inputs
     constexpr int TMM = TmaTm<P>::value ? 1 : (TmaTmEpi<P>::value ? 2 : 0);
@@ -247,6 +260,7 @@ inline int launch_sweep(Ctx* c, P& p, const HaloOut* hout = nullptr) {
       sweep_tma_kernel<P><<<nb, NTH, smem, c->stream>>>(p);
     prof_end(c);
   } else {
+    if constexpr (HasSide<P>::value) return set_error("z-lag pass off the TMA sweep path", GADI_ERR_ARG);
     p.g = make_geom(c, S::TZ, S::TY, P::VZ);
     const int nb = geom_blocks(p.g);
     if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
@@ -531,6 +545,13 @@ struct Engine {
     hi.maxit = maxit;
     GADI_TRY(launch_pw(c, hi));
     GADI_TRY(halo(c, c->R, sizeof(ST)));
+    // z-lag (passes.cuh HcgA): only where every H-CG pass runs the barrier-free form
+    if (zlag_ok<HcgA<G, false, RF, true>>(c) && zlag_ok<HcgB<G, RF, true>>(c))
+      return h_loop_t<G, RF, true>(c, maxit);
+    return h_loop_t<G, RF, false>(c, maxit);
+  }
+  template <class G, bool RF, bool ZL>
+  static int h_loop_t(Ctx* c, int maxit) {
     const CoefT<CT> H = cast_coef<CT>(c->H);
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
     auto iter = [&](int k) -> int {
@@ -546,17 +567,18 @@ struct Engine {
           hf = halo_begin(c, P[1], sizeof(ST), ho);
           GADI_TRY(launch_sweep(c, a, &ho));
         } else {
-          HcgA<G, false, RF> a;
+          HcgA<G, false, RF, ZL> a;
           a.st = c->hst;
           a.r = (const ST*)c->R;
           a.pin = P[k & 1];
           a.pout = P[(k + 1) & 1];
+          a.z = (ST*)c->Z;
           a.H = H;
           hf = halo_begin(c, P[(k + 1) & 1], sizeof(ST), ho);
           GADI_TRY(launch_sweep(c, a, &ho));
         }
         GADI_TRY(halo_end(c, P[(k + 1) & 1], sizeof(ST), hf));
-        HcgB<G, RF> b;
+        HcgB<G, RF, ZL> b;
         b.st = c->hst;
         b.p = P[(k + 1) & 1];
         b.z = (ST*)c->Z;
@@ -576,6 +598,14 @@ struct Engine {
       GADI_TRY(run_loop_graph(c, c->gexec_h, c->hst, c->h_hst, c->pred_h, 2));
     } else {
       GADI_TRY(run_batched(c, c->hst, c->h_hst, c->pred_h, maxit, iter));
+    }
+    if constexpr (ZL) {
+      HcgZFinal<ST, RF> zf;
+      zf.st = c->hst;
+      zf.P0 = P[0];
+      zf.P1 = P[1];
+      zf.z = (ST*)c->Z;
+      GADI_TRY(launch_pw(c, zf));
     }
     return halo(c, c->Z, sizeof(ST));  // z is the stencil input of the CGNR init
   }

@@ -25,6 +25,20 @@ namespace gadi {
 #ifndef GADI_VZNORM
 #define GADI_VZNORM 4  // fp64 elements per lane (measured: 4 beats 2 here, not in the other fp64 passes)
 #endif
+// GADI_NORM_MBAR = 1: the per-plane CTA barrier between "t-plane x+1 stored"
+// and "A^T reads t-plane x" becomes one mbarrier per t buffer (4 buffers):
+// every consumer / helper warp arrives after storing its part of a t-plane
+// and waits only for the plane it is about to read (stored one plane
+// earlier), so warps drift within the ring instead of meeting every plane.
+#ifndef GADI_NORM_MBAR
+#define GADI_NORM_MBAR 0
+#endif
+// GADI_NORM_ILP = 1: the 7-term stencils as two independent FMA chains
+// (depth 4 instead of 7) and one ||w'||^2 accumulator per vector element
+// (the fp64 chain through `red` was one dependent DFMA per element)
+#ifndef GADI_NORM_ILP
+#define GADI_NORM_ILP 0
+#endif
 template <int DIM>
 struct NFShape {
   static constexpr int VZ = GADI_VZNORM;
@@ -46,11 +60,12 @@ struct NFShape {
   static constexpr int NH = DIM == 3 ? 2 : 1;
   static constexpr int NCONS = NT + 32 * NH;
   static constexpr int NTOT = NCONS + 32;
-  static constexpr int TBYTES = (3 * TPLANE * 8 + 127) / 128 * 128;  // stages 128-byte aligned (TMA boxes)
+  static constexpr int NTB = GADI_NORM_MBAR ? 4 : 3;              // t buffers
+  static constexpr int TBYTES = (NTB * TPLANE * 8 + 127) / 128 * 128;  // stages 128-byte aligned (TMA boxes)
   static constexpr int BUDGET = 100 * 1024;
   static constexpr int NST_RAW = (BUDGET - TBYTES) / STAGE;
   static constexpr int NST = NST_RAW >= 8 ? 8 : 4;  // power of two: cheap stage indexing
-  static constexpr size_t SMEM = (size_t)TBYTES + (size_t)NST * STAGE + 2 * NST * sizeof(uint64_t);
+  static constexpr size_t SMEM = (size_t)TBYTES + (size_t)NST * STAGE + (2 * NST + NTB) * sizeof(uint64_t);
 };
 
 template <int DIM, bool DENSE>
@@ -88,7 +103,15 @@ struct NormFused {
 template <int DIM, bool DENSE>
 __device__ __forceinline__ double nf_stencil(const CoefT<double>& c, double xm, double ym, double zm, double ce,
                                              double zp, double yp, double xp) {
-  if constexpr (DENSE && !GADI_NORM_ORDERED) {
+  if constexpr (DENSE && !GADI_NORM_ORDERED && GADI_NORM_ILP) {
+    double a = c.lo[0] * xm, b = c.up[0] * xp;
+    a = fma_rn(c.lo[1], ym, a);
+    b = fma_rn(c.up[1], yp, b);
+    a = fma_rn(c.lo[2], zm, a);
+    b = fma_rn(c.up[2], zp, b);
+    a = fma_rn(c.d, ce, a);
+    return a + b;
+  } else if constexpr (DENSE && !GADI_NORM_ORDERED) {
     double acc = c.lo[0] * xm;
     acc = fma_rn(c.lo[1], ym, acc);
     acc = fma_rn(c.lo[2], zm, acc);
@@ -114,6 +137,7 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
   unsigned char* stages = smem_raw + S::TBYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)NST * S::STAGE);
   uint64_t* empty = full + NST;
+  uint64_t* twr = empty + NST;  // GADI_NORM_MBAR: "t buffer b stored" (all consumer + helper warps)
 
   if (!p.prepare()) return;
   const SweepGeom g = p.g;
@@ -123,10 +147,14 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWCONS);
     }
+    for (int b = 0; b < S::NTB; ++b) mbar_init(&twr[b], NWCONS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   double red[1] = {0.0};
+  double redk[VZ];
+#pragma unroll
+  for (int k = 0; k < VZ; ++k) redk[k] = 0.0;
 
   if (tid >= NCONS) {
     // ---------------------------------------------------------------- producer
@@ -192,6 +220,7 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
 
     SegIter it(g, gridDim.x, blockIdx.x);
     int tile, xa, xb, gs = 0;
+    int tq = 0;  // GADI_NORM_MBAR: t-planes stored by this CTA before the segment
     while (it.next(tile, xa, xb)) {
       const int zt0 = (tile % g.nzt) * TZ, y0 = (tile / g.nzt) * TY;
       const int y = y0 + trow - HT;
@@ -255,8 +284,25 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
                                       vat(s, x + 1, vr, c - 1), vat(s, x + 1, vr, c), vat(s, x + 1, vr, c + 1),
                                       vat(s, x + 1, vr + 1, c), vat(st_of(x + 2), x + 2, vr, c)) * rnw;
       };
-      auto t_store = [&](int x, const double (&t)[VZ]) {  // t-plane x+1 -> buffer (x+1) % 3
-        double* b = tbuf + (size_t)(((x + 1) - (xa - 1)) % 3) * S::TPLANE + HZ;
+      // t-plane x (x >= xa) is the CTA's stored plane tq + x - xa
+      auto tbuf_of = [&](int x) -> double* {
+        if constexpr (GADI_NORM_MBAR) return tbuf + (size_t)((tq + x - xa) % S::NTB) * S::TPLANE + HZ;
+        else return tbuf + (size_t)((x - (xa - 1)) % 3) * S::TPLANE + HZ;
+      };
+      auto t_published = [&](int x) {  // this warp's part of t-plane x is in its buffer
+        if constexpr (GADI_NORM_MBAR) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&twr[(tq + x - xa) % S::NTB]);
+        }
+      };
+      auto t_wait = [&](int x) {  // every warp's part of t-plane x is in its buffer
+        if constexpr (GADI_NORM_MBAR) {
+          const int q = tq + x - xa;
+          mbar_wait(&twr[q % S::NTB], (unsigned)((q / S::NTB) & 1));
+        }
+      };
+      auto t_store = [&](int x, const double (&t)[VZ]) {  // t-plane x+1 -> its buffer
+        double* b = tbuf_of(x + 1);
         if (has_row) {
 #pragma unroll
           for (int k = 0; k < VZ; ++k) b[(size_t)trow * ROW + tz * VZ + k] = t[k];
@@ -282,9 +328,13 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
       wait_full(st_of(xa + 1));
       vown(xa + 1, vC);
       t_own(xa - 1, vA, vB, vC, tc);
+      // (mbarrier form) the buffers this segment overwrites first were last
+      // read before every warp stored the previous segment's final t-plane
+      if (GADI_NORM_MBAR && tq > 0) t_wait(xa - 1);
       t_store(xa - 1, tc);
+      t_published(xa);
       release(st_of(xa - 1));
-      consumer_sync(NCONS);
+      if constexpr (!GADI_NORM_MBAR) consumer_sync(NCONS);
 
       long long gidx = (long long)xa * g.plane + (long long)y * g.nz + zb;
       for (int x = xa; x < xb; ++x, gidx += g.plane) {
@@ -298,14 +348,20 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
         vown(x + 2, vC);
         t_own(x, vA, vB, vC, tn);
         t_store(x, tn);
-        consumer_sync(NCONS);
-        release(st_of(x));
+        if constexpr (GADI_NORM_MBAR) {
+          t_published(x + 1);
+          release(st_of(x));
+          t_wait(x);
+        } else {
+          consumer_sync(NCONS);
+          release(st_of(x));
+        }
         // w'-plane x = A^T t from t(x-1), t(x), t(x+1)
         if (!halo) {
           double left = __shfl_up_sync(0xffffffffu, tc[VZ - 1], 1);
           double right = __shfl_down_sync(0xffffffffu, tc[0], 1);
           if (own) {
-            const double* b = tbuf + (size_t)((x - (xa - 1)) % 3) * S::TPLANE + HZ;
+            const double* b = tbuf_of(x);
             const double* rc = b + (size_t)trow * ROW + tz * VZ;
             const double* rm = rc - ROW;
             const double* rp = rc + ROW;
@@ -319,7 +375,8 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
               const double ym = DIM == 3 ? rm[k] : 0.0;
               const double yp = DIM == 3 ? rp[k] : 0.0;
               o[k] = nf_stencil<DIM, DENSE>(p.AT, tp[k], ym, zm, tc[k], zp, yp, tn[k]);
-              red[0] += o[k] * o[k];
+              if constexpr (GADI_NORM_ILP) redk[k] = fma_rn(o[k], o[k], redk[k]);
+              else red[0] += o[k] * o[k];
             }
             store_any<double, VZ>(p.outv, gidx, VZ, o, true);
           }
@@ -333,7 +390,12 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
       release(st_of(xb));
       release(st_of(xb + 1));
       gs += xb - xa + 4;
+      tq += xb - xa + 1;
     }
+  }
+  if constexpr (GADI_NORM_ILP) {
+#pragma unroll
+    for (int k = 0; k < VZ; ++k) red[0] += redk[k];
   }
 
   double tot[1];

@@ -63,7 +63,7 @@ struct GeoT {
 // Kernel ids for the live per-kernel timers (gadi_prof_*).
 enum KernelId {
   K_HCG_INIT = 0, K_HCG_A, K_HCG_B, K_CGNR_INIT, K_CGNR_P1, K_CGNR_P2, K_CGNR_P3,
-  K_C_INIT, K_C_P1, K_C_P2, K_OUTER, K_NORM_A, K_NORM_B, K_APPLY, K_TREE, K_NKID
+  K_C_INIT, K_C_P1, K_C_P2, K_OUTER, K_NORM_A, K_NORM_B, K_APPLY, K_TREE, K_HCG_Z, K_NKID
 };
 
 struct InnerState {
@@ -347,11 +347,20 @@ struct PassBase {
 // f = (it == 0) ? r : round(r + beta p_in) ; Hf ; store p_out ; sum f.Hf
 // RF (all CG / CGNR passes): the reference's per-operation rounding
 // (strict.cuh) instead of the storage model; TS is the pass's fl_dot slot.
-template <class G, bool FIRST = false, bool RF = false>
+// Z-lag (GADI_ZLAG, engine.cuh): the CG update z += alpha_k p_k of inner.py:74
+// moves from HcgB(k) to HcgA(k+1), which holds p_k as its raw input anyway:
+// at field time the consumer rounds z + alpha_k p_k for its own rows
+// (`side`, z staged as an epilogue row) and stores it.  HcgB keeps only the
+// r update, and HcgZFinal (pointwise.cuh) applies the last iteration's
+// update after the loop.  Same values, same rounding, same order of updates
+// per element; it moves 4 B/n of traffic from the DRAM-bound HcgB to the
+// issue-bound HcgA.
+template <class G, bool FIRST = false, bool RF = false, bool ZL = false>
 struct HcgA : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
   static constexpr int NF = 1, NR = 1;
+  static constexpr bool SIDE = ZL && !FIRST;  // z += alpha_prev p_in at field time
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
   static constexpr int TS = (RF && !ORD) ? 0 : -1;
   static constexpr int KID = K_HCG_A;
@@ -360,8 +369,10 @@ struct HcgA : G, PassBase {
   const ST* r;
   const ST* pin;
   ST* pout;
+  ST* z;     // SIDE: z, updated in place with alpha_{k-1} p_{k-1}
   CoefT<CT> H;
   CT beta;
+  CT alpha;  // SIDE: alpha_{k-1} (HcgA(k)'s own finalize writes alpha_k after every CTA read it)
   static constexpr bool first = FIRST;  // iteration 0: p = r, p_in is not read
   // sweep_tma2 in-place form: the rounded p is written over the raw p row
   static constexpr bool INPLACE = !FIRST;
@@ -372,7 +383,18 @@ struct HcgA : G, PassBase {
   __device__ bool prepare() {
     if (st->done) return false;
     beta = (CT)st->beta;
+    if constexpr (SIDE) alpha = (CT)st->alpha;
     return true;
+  }
+  // SIDE: z(i..i+VZ) = round(z + alpha p_in) from the raw inputs of an owned row
+  // (inner.py:74 of the previous iteration; E = the row's staged z)
+  __device__ void side(const Raw& a, const SmRow& E, int zo, long long i) const {
+    if constexpr (SIDE) {
+      CT zv[G::VZ], zn[G::VZ];
+      lds_vec<ST, G::VZ>(E.p[0], zo, zv);
+      axpy_m<ST, RF>(alpha, a.p, zv, zn);
+      store_exact<ST, G::VZ>(z, i, G::VZ, zn, g.vec);
+    }
   }
   __device__ void field_vec(const Raw& a, CT (&f)[1][G::VZ]) const {
     if constexpr (FIRST) {
@@ -383,11 +405,11 @@ struct HcgA : G, PassBase {
     }
   }
   GADI_STENCIL_VEC(H)
-  static constexpr int NIN = 2, NE = 0;
+  static constexpr int NIN = 2, NE = SIDE ? 1 : 0;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
-  static constexpr int epi_esz(int) { return 1; }
+  static constexpr int epi_esz(int) { return SIDE ? (int)sizeof(ST) : 1; }
   __host__ __device__ const void* in_ptr(int j) const { return j == 0 ? (const void*)r : (const void*)pin; }
-  __host__ __device__ const void* epi_ptr(int) const { return nullptr; }
+  __host__ __device__ const void* epi_ptr(int) const { return SIDE ? (const void*)z : nullptr; }
   __host__ __device__ bool in_active(int j) const { return j == 0 || !first; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int z) const {
     lds_vec<ST, G::VZ>(R.p[0], z, a.r);
@@ -428,10 +450,11 @@ struct HcgA : G, PassBase {
 };
 
 // f = p ; Hp ; z += alpha p ; r -= alpha Hp ; sum r.r ; convergence, beta
-template <class G, bool RF = false>
+template <class G, bool RF = false, bool ZL = false>
 struct HcgB : G, PassBase {
   typedef typename G::CT CT;
   typedef typename G::ST ST;
+  static constexpr bool ZLAG = ZL;  // z update moved to the next HcgA / HcgZFinal
   static constexpr int NF = 1, NR = 1;
   static constexpr bool HAS_RED = true, ORD = std::is_same<ST, double>::value, TMA_OK = true;
   static constexpr int TS = (RF && !ORD) ? 0 : -1;
@@ -445,31 +468,38 @@ struct HcgB : G, PassBase {
   CT alpha;
   struct Raw { CT p[G::VZ]; };
   struct RawS { CT p; };
-  struct Epi { CT z[G::VZ], r[G::VZ]; };
+  struct Epi { CT z[ZL ? 1 : G::VZ], r[G::VZ]; };
   __device__ bool prepare() {
     if (st->done) return false;
     alpha = (CT)st->alpha;
     return true;
   }
   GADI_STENCIL_VEC(H)
-  static constexpr int NIN = 1, NE = 2;
+  static constexpr int NIN = 1, NE = ZL ? 1 : 2;
   static constexpr int in_esz(int) { return (int)sizeof(ST); }
   static constexpr int epi_esz(int) { return (int)sizeof(ST); }
   __host__ __device__ const void* in_ptr(int) const { return p; }
-  __host__ __device__ const void* epi_ptr(int j) const { return j == 0 ? (const void*)z : (const void*)r; }
+  __host__ __device__ const void* epi_ptr(int j) const {
+    if constexpr (ZL) return (const void*)r;
+    return j == 0 ? (const void*)z : (const void*)r;
+  }
   __host__ __device__ bool in_active(int) const { return true; }
   __device__ void load_raw_sm(Raw& a, const SmRow& R, int zo) const { lds_vec<ST, G::VZ>(R.p[0], zo, a.p); }
   __device__ void load_raw_s_sm(RawS& a, const SmRow& R, int zo) const { a.p = lds1<ST, CT>(R.p[0], zo); }
   __device__ void load_epi_sm(Epi& e, const SmRow& R, int zo) const {
-    lds_vec<ST, G::VZ>(R.p[0], zo, e.z);
-    lds_vec<ST, G::VZ>(R.p[1], zo, e.r);
+    if constexpr (ZL) {
+      lds_vec<ST, G::VZ>(R.p[0], zo, e.r);
+    } else {
+      lds_vec<ST, G::VZ>(R.p[0], zo, e.z);
+      lds_vec<ST, G::VZ>(R.p[1], zo, e.r);
+    }
   }
   __device__ void load_raw(Raw& a, long long i, int nv) const { load_any<ST, G::VZ, true>(p, i, nv, a.p, g.vec); }
   __device__ void load_raw_s(RawS& a, long long i) const { a.p = cvt_in<CT>(p[i]); }
   __device__ void field(const Raw& a, int k, CT (&f)[1]) const { f[0] = a.p[k]; }
   __device__ void field_s(const RawS& a, CT (&f)[1]) const { f[0] = a.p; }
   __device__ void load_epi(Epi& e, long long i, int nv) const {
-    load_any<ST, G::VZ, false>(z, i, nv, e.z, g.vec);
+    if constexpr (!ZL) load_any<ST, G::VZ, false>(z, i, nv, e.z, g.vec);
     load_any<ST, G::VZ, false>(r, i, nv, e.r, g.vec);
   }
   __device__ CT stencil(int, int, const Nb<CT>& n, const CT (&)[1][G::VZ], const Epi&) const {
@@ -477,13 +507,16 @@ struct HcgB : G, PassBase {
   }
   __device__ void epilogue(long long i, int nv, const CT (&fc)[1][G::VZ], const CT (&s)[1][G::VZ], const Epi& e,
                            double (&red)[1]) const {
-    CT zn[G::VZ], rn[G::VZ], hp[G::VZ];
+    CT rn[G::VZ], hp[G::VZ];
     round_vec_m<ST, RF>(s[0], hp);
-    axpy_m<ST, RF>(alpha, fc[0], e.z, zn);   // inner.py:74
+    if constexpr (!ZL) {
+      CT zn[G::VZ];
+      axpy_m<ST, RF>(alpha, fc[0], e.z, zn);  // inner.py:74
+      store_exact<ST, G::VZ>(z, i, nv, zn, g.vec);
+    }
     axpy_m<ST, RF>(-alpha, hp, e.r, rn);     // inner.py:75
     if constexpr (TS >= 0) red[0] = dot_leaf<G::VZ, (G::ZS == 2 ? 1 : 0)>(tout, i, nv, rn, rn);  // inner.py:76
     else red[0] += dotv<CT, G::VZ>(rn, rn, nv);
-    store_exact<ST, G::VZ>(z, i, nv, zn, g.vec);
     store_out<ST, G::VZ>(hout, g, r, i, nv, rn);
   }
   __device__ void finalize(const double (&t)[1]) const { fin_cg_beta(st, t[0], ScalarRnd<ST, RF>::value); }

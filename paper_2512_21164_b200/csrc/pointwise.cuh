@@ -116,6 +116,42 @@ struct HcgInit : PwBase {
   }
 };
 
+// Z-lag (GADI_ZLAG, passes.cuh HcgA): the last CG iteration's z += alpha p
+// (inner.py:74), after the loop.  The iteration count and the breakdown flag
+// select it: K = it - 1 iterations ran their HcgB (p_K in P[it & 1]); a
+// breakdown in HcgA(K) returns before the update (inner.py:70-72), as does a
+// loop that never started.
+template <class ST, bool RF = false>
+struct HcgZFinal : PwBase {
+  typedef typename CTOf<ST>::type CT;
+  static constexpr int VZ = (int)(16 / sizeof(ST)) >= 2 ? (int)(16 / sizeof(ST)) : 2;
+  static constexpr int NR = 1;
+  static constexpr int TS = -1;
+  static constexpr bool HAS_RED = false;
+  static constexpr int KID = K_HCG_Z;
+  static __device__ __forceinline__ int op(int) { return RED_SUM; }
+  const InnerState* st;
+  const ST* P0;
+  const ST* P1;
+  ST* z;
+  const ST* p;
+  CT alpha;
+  __device__ bool prepare() {
+    if (st->breakdown || st->it <= 0) return false;
+    alpha = (CT)st->alpha;
+    p = (st->it & 1) ? P1 : P0;
+    return true;
+  }
+  __device__ void apply(long long i, int nv, double (&)[1]) const {
+    CT pv[VZ], zv[VZ], zn[VZ];
+    load_any<ST, VZ, true>(p, i, nv, pv, true);
+    load_any<ST, VZ, false>(z, i, nv, zv, true);
+    axpy_m<ST, RF>(alpha, pv, zv, zn);
+    store_exact<ST, VZ>(z, i, nv, zn, true);
+  }
+  __device__ void finalize(const double (&)[1]) const {}
+};
+
 // ---------------------------------------------------------------- complex S
 // Interleaved pairs (re, im).  S (a + ib) = (alpha a - v b) + i (v a + alpha b),
 // S^T = alpha I - N flips the sign of v.  Accumulation order follows the CSR

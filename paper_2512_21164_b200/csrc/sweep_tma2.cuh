@@ -53,6 +53,13 @@ template <class P>
 struct HasInplace<P, std::void_t<decltype(P::INPLACE)>>
     : std::integral_constant<bool, P::INPLACE && GADI_INPLACE != 0 && P::NF == 1 && (SweepShape<P>::BY > 1)> {};
 
+// Passes with a field-time side update of their own rows (HcgA under
+// GADI_ZLAG: z += alpha p_in, passes.cuh); barrier-free form only.
+template <class P, class = void>
+struct HasSide : std::false_type {};
+template <class P>
+struct HasSide<P, std::void_t<decltype(P::SIDE)>> : std::integral_constant<bool, P::SIDE> {};
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -300,6 +307,24 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
           for (int q = 0; q < NF; ++q) f[q][k] = CT(0);
       }
     };
+    // fields of this lane's own row (stage row ty + 1), plus the pass's side
+    // update of the owned plane (element index i) when `side`
+    auto own_fields_at = [&](int st, bool ok, bool side, long long i, CT (&f)[NF][VZ]) {
+      if constexpr (HasSide<P>::value) {
+        static_assert(!GADI_EPI_LDG, "side updates read the staged epilogue row");
+        if (ok) {
+          typename P::Raw a;
+          p.load_raw_sm(a, in_row(st, ty + 1), tz * VZ);
+          p.field_vec(a, f);
+          if (side) p.side(a, epi_row(st, ty), tz * VZ, i);
+        } else {
+#pragma unroll
+          for (int k = 0; k < VZ; ++k) f[0][k] = CT(0);
+        }
+      } else {
+        fields_at(st, ty + 1, ok, f);
+      }
+    };
     // scalar field at element offset zo of stage row r (z-edges)
     auto field_scalar = [&](int st, int r, int zo, bool ok, CT (&f)[NF]) {
       if (ok) {
@@ -352,11 +377,11 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
       release(ps);
       ps.next();  // plane xa
       wait_full(ps);
-      fields_at(ps.slot, ty + 1, own, fcur);
+      long long gidx = (long long)xa * g.plane + rowbase;
+      own_fields_at(ps.slot, own, own, gidx, fcur);
       put_field(ps.slot, fcur);
       Pos pn = ps;
 
-      long long gidx = (long long)xa * g.plane + rowbase;
 #if GADI_EPI_LDG
       typename P::Epi En;
       if (own) p.load_epi(En, gidx, VZ);
@@ -373,7 +398,7 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
         const int s = ps.slot;  // stage slot of plane x
         pn.next();              // plane x+1
         wait_full(pn);
-        fields_at(pn.slot, ty + 1, own && x + 1 < g.nx + g.hhi, fnext);
+        own_fields_at(pn.slot, own && x + 1 < g.nx + g.hhi, own && x + 1 < xb, gidx + g.plane, fnext);
         put_field(pn.slot, fnext);
         CT fym[NF][VZ], fyp[NF][VZ];
         if constexpr (INPL) {

@@ -26,7 +26,8 @@ real = {"hcg_a": ih, "hcg_b": ih, "cgnr_p1": is_, "cgnr_p2": is_, "cgnr_p3": max
         "norm_a": rep.norm_iterations, "outer": rep.iterations + 1, "hcg_init": rep.iterations,
         "cgnr_init": rep.iterations}
 # per launch that did work (no-op launches past convergence included in the time)
-print(json.dumps({"knobs": knobs, "ng": ng, "us": us,
+print(json.dumps({"knobs": knobs, "ng": ng, "us": us, "norm_A": rep.norm_A, "norm_iterations": rep.norm_iterations,
+                  "relres": [h.relative_residual for h in rep.history],
                   "kernels": {k: round(ms / max(1, min(n, real.get(k, n))) * 1e3, 2) for k, (ms, n) in prof.items()},
                   "launches": {k: n for k, (ms, n) in prof.items()}, "real": real,
                   "total_ms": {k: round(ms, 2) for k, (ms, n) in prof.items()}}))

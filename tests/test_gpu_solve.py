@@ -255,3 +255,36 @@ def test_fp16_solves(gpu, name):
     assert [h.inner_s_iterations for h in ex.history] == c["inner_s"]
     # (the non-converged fp16 runs overflow to NaN in the reference too)
     assert np.array_equal(ex.x[:8], np.array(c["x_head"]), equal_nan=True)
+
+
+_ZLAG_PROBE = r"""
+import json, sys
+import numpy as np
+import paper_2512_21164_b200 as g
+out = []
+for rounding, us in (("storage", "bf16"), ("reference", "bf16"), ("storage", "fp32")):
+    cfg = g.GadiConfig(alpha=0.3, u_s=us, outer_tol=1e-10, outer_maxit=60, inner_tol=1e-3, strict_model=False)
+    rep = g.gadi_solve(g.build_cd_3d(32), cfg=cfg, rounding=rounding)
+    out.append({"status": rep.status, "relres": [h.relative_residual for h in rep.history],
+                "inner": [h.inner_h_iterations for h in rep.history],
+                "x": float(np.sum(np.asarray(rep.x, dtype=np.float64) ** 2))})
+print(json.dumps(out))
+"""
+
+
+def test_zlag_form_bitwise_default(gpu):
+    """GADI_ZLAG=1 (z += alpha p moved from HcgB(k) into HcgA(k+1) plus a
+    final pass, engine.cuh zlag_ok) is the same arithmetic: identical
+    histories and iterates in both rounding models."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    res = {}
+    for zl in ("0", "1"):
+        env = dict(os.environ, GADI_ZLAG=zl)
+        p = subprocess.run([sys.executable, "-c", _ZLAG_PROBE], env=env, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[zl] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["0"] == res["1"]
