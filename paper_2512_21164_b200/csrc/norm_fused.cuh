@@ -10,8 +10,9 @@
 // y-halo rows and the two z-halo columns) from the v-planes
 // x, x+1, x+2 held in the TMA stage ring, keeps t for its own columns in a
 // 3-plane register queue (x-neighbours) and the whole t-plane in a
-// triple-buffered shared-memory plane (y / z neighbours), and applies A^T to
-// produce w'-plane x.
+// shared-memory ring of t-planes (y / z neighbours; 3-D: four planes handed
+// over by one mbarrier each, 2-D: three behind a CTA barrier), and applies
+// A^T to produce w'-plane x.
 //
 // Real 5-point (DIM 2: rows of 64 lanes) and 7-point (DIM 3: 32 lanes x TY
 // rows) stencils on a single domain; the crd family and slab contexts keep
@@ -31,7 +32,7 @@ namespace gadi {
 // and waits only for the plane it is about to read (stored one plane
 // earlier), so warps drift within the ring instead of meeting every plane.
 #ifndef GADI_NORM_MBAR
-#define GADI_NORM_MBAR 0
+#define GADI_NORM_MBAR 1
 #endif
 // GADI_NORM_ILP = 1: the 7-term stencils as two independent FMA chains
 // (depth 4 instead of 7) and one ||w'||^2 accumulator per vector element
@@ -39,11 +40,30 @@ namespace gadi {
 #ifndef GADI_NORM_ILP
 #define GADI_NORM_ILP 0
 #endif
+#ifndef GADI_NORM_XU
+#define GADI_NORM_XU 1
+#endif
+// tile rows, CTAs per SM (register budget) and stage-count rule of the fused
+// power iteration (GADI_NORM_NSTANY = 0: 8 or 4 stages, a power of two)
+// 3-D default: 16-row tiles, one CTA per SM (107 registers: the mbarrier
+// form no longer spills) -- 782 -> 708 us at 512^3 (profiles/ab_norm_tile2_r2.jsonl);
+// 2-D keeps 2 CTAs per SM of one-row tiles and the CTA barrier.
+#ifndef GADI_NORM_TY
+#define GADI_NORM_TY 16
+#endif
+#ifndef GADI_NORM_MINB
+#define GADI_NORM_MINB 1
+#endif
+#ifndef GADI_NORM_NSTANY
+#define GADI_NORM_NSTANY 0
+#endif
 template <int DIM>
 struct NFShape {
   static constexpr int VZ = GADI_VZNORM;
   static constexpr int BZ = DIM == 3 ? 32 : 64;
-  static constexpr int TY = DIM == 3 ? GADI_BY3 : 1;
+  static constexpr int TY = DIM == 3 ? GADI_NORM_TY : 1;
+  static constexpr int MINB = DIM == 3 ? GADI_NORM_MINB : 2;  // CTAs per SM (register budget)
+  static constexpr bool MB = GADI_NORM_MBAR && DIM == 3;      // mbarrier t-plane handoff
   static constexpr int TZ = BZ * VZ;
   static constexpr int HZ = 2;                       // 16-byte pad = 2 fp64 each side
   static constexpr int HV = DIM == 3 ? 2 : 0;        // v halo rows each side
@@ -60,11 +80,12 @@ struct NFShape {
   static constexpr int NH = DIM == 3 ? 2 : 1;
   static constexpr int NCONS = NT + 32 * NH;
   static constexpr int NTOT = NCONS + 32;
-  static constexpr int NTB = GADI_NORM_MBAR ? 4 : 3;              // t buffers
+  static constexpr int NTB = MB ? 4 : 3;                          // t buffers
   static constexpr int TBYTES = (NTB * TPLANE * 8 + 127) / 128 * 128;  // stages 128-byte aligned (TMA boxes)
-  static constexpr int BUDGET = 100 * 1024;
+  static constexpr int BUDGET = (MINB >= 3 ? 72 : (MINB >= 2 ? 100 : 200)) * 1024;
   static constexpr int NST_RAW = (BUDGET - TBYTES) / STAGE;
-  static constexpr int NST = NST_RAW >= 8 ? 8 : 4;  // power of two: cheap stage indexing
+  static constexpr int NST = GADI_NORM_NSTANY ? (NST_RAW > 8 ? 8 : NST_RAW)
+                                              : (NST_RAW >= 8 ? 8 : 4);  // power of two: cheap stage indexing
   static constexpr size_t SMEM = (size_t)TBYTES + (size_t)NST * STAGE + (2 * NST + NTB) * sizeof(uint64_t);
 };
 
@@ -127,7 +148,7 @@ __device__ __forceinline__ double nf_stencil(const CoefT<double>& c, double xm, 
 }
 
 template <int DIM, bool DENSE>
-__global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
+__global__ void __launch_bounds__(NFShape<DIM>::NTOT, NFShape<DIM>::MINB)
     norm_fused_kernel(NormFused<DIM, DENSE> p, const __grid_constant__ CUtensorMap tmw) {
   using S = NFShape<DIM>;
   constexpr int VZ = S::VZ, BZ = S::BZ, TY = S::TY, TZ = S::TZ, HZ = S::HZ, HV = S::HV, HT = S::HT;
@@ -286,17 +307,17 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
       };
       // t-plane x (x >= xa) is the CTA's stored plane tq + x - xa
       auto tbuf_of = [&](int x) -> double* {
-        if constexpr (GADI_NORM_MBAR) return tbuf + (size_t)((tq + x - xa) % S::NTB) * S::TPLANE + HZ;
+        if constexpr (S::MB) return tbuf + (size_t)((tq + x - xa) % S::NTB) * S::TPLANE + HZ;
         else return tbuf + (size_t)((x - (xa - 1)) % 3) * S::TPLANE + HZ;
       };
       auto t_published = [&](int x) {  // this warp's part of t-plane x is in its buffer
-        if constexpr (GADI_NORM_MBAR) {
+        if constexpr (S::MB) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&twr[(tq + x - xa) % S::NTB]);
         }
       };
       auto t_wait = [&](int x) {  // every warp's part of t-plane x is in its buffer
-        if constexpr (GADI_NORM_MBAR) {
+        if constexpr (S::MB) {
           const int q = tq + x - xa;
           mbar_wait(&twr[q % S::NTB], (unsigned)((q / S::NTB) & 1));
         }
@@ -330,13 +351,19 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
       t_own(xa - 1, vA, vB, vC, tc);
       // (mbarrier form) the buffers this segment overwrites first were last
       // read before every warp stored the previous segment's final t-plane
-      if (GADI_NORM_MBAR && tq > 0) t_wait(xa - 1);
+      if (S::MB && tq > 0) t_wait(xa - 1);
       t_store(xa - 1, tc);
       t_published(xa);
       release(st_of(xa - 1));
-      if constexpr (!GADI_NORM_MBAR) consumer_sync(NCONS);
+      if constexpr (!S::MB) consumer_sync(NCONS);
 
       long long gidx = (long long)xa * g.plane + (long long)y * g.nz + zb;
+      // GADI_NORM_XU = 3 unrolls by the period of the v / t register queues
+#if GADI_NORM_XU == 3
+#pragma unroll 3
+#elif GADI_NORM_XU == 2
+#pragma unroll 2
+#endif
       for (int x = xa; x < xb; ++x, gidx += g.plane) {
         // t-plane x+1 from v-planes x, x+1, x+2
 #pragma unroll
@@ -348,7 +375,7 @@ __global__ void __launch_bounds__(NFShape<DIM>::NTOT, 2)
         vown(x + 2, vC);
         t_own(x, vA, vB, vC, tn);
         t_store(x, tn);
-        if constexpr (GADI_NORM_MBAR) {
+        if constexpr (S::MB) {
           t_published(x + 1);
           release(st_of(x));
           t_wait(x);
