@@ -125,8 +125,8 @@ __device__ void inplace_halo_rows(const P& p, const SweepGeom& g, unsigned char*
         // the z-neighbour fields just outside the tile (columns -1 and TZ) of
         // every row, so the consumers' edge lanes load them instead of
         // evaluating the field in a divergent branch
-        if (lane < 2 * (TY + 2)) {
-          const int r = lane >> 1, right = lane & 1;
+        for (int q = lane; q < 2 * (TY + 2); q += 32) {
+          const int r = q >> 1, right = q & 1;
           const int tzl = right ? BZ_ - 1 : 0, zo = right ? TZ : -1;
           const int zz = zt0 + zo, yy = y0 - 1 + r;
           const bool ok = zz >= 0 && zz < g.nz && yy >= 0 && yy < g.ny;
