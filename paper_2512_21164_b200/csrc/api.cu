@@ -417,6 +417,7 @@ static int ctx_create(const gadi_problem_desc* desc, int device, gadi_comm* comm
   if (getenv("GADI_WAVEFRONT")) c->wavefront = atoi(getenv("GADI_WAVEFRONT"));
   if (getenv("GADI_BATCH_CAP")) c->batch_cap = std::max(0, atoi(getenv("GADI_BATCH_CAP")));
   if (getenv("GADI_TMA2")) c->tma2 = atoi(getenv("GADI_TMA2"));
+  if (getenv("GADI_TALL")) c->tall = atoi(getenv("GADI_TALL"));
   if (getenv("GADI_ZLAG")) c->zlag_on = atoi(getenv("GADI_ZLAG")) != 0;
   if (getenv("GADI_TMAP")) c->tmap = atoi(getenv("GADI_TMAP"));
   if (getenv("GADI_TM_PROMO")) c->tm_promo = atoi(getenv("GADI_TM_PROMO"));

@@ -119,6 +119,7 @@ struct Ctx {
   int wavefront = 0;  // wavefront schedule (one CTA per tile) when the tiles fit in one wave
   int batch_cap = 0;  // max inner iterations enqueued per poll (0: the adaptive batch alone)
   int tma2 = 1;       // barrier-free TMA consumers (sweep_tma2.cuh); 0: f-plane form
+  int tall = 1;       // GADI_TALL=0: HcgA keeps the default 8-row tiles (passes.cuh GeoT TALL)
   int zlag_on = 0;    // GADI_ZLAG=1: z updated in the next HcgA (engine.cuh zlag_ok)
   // device-driven inner loops: CUDA graphs whose conditional WHILE node
   // repeats two captured iterations until the solve state is done

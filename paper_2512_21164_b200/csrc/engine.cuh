@@ -204,6 +204,9 @@ inline int launch_sweep(Ctx* c, P& p, const HaloOut* hout = nullptr) {
     if constexpr (HasSide<P>::value) {
       if (!v2) return set_error("z-lag pass off the barrier-free sweep form", GADI_ERR_ARG);
     }
+    if constexpr (P::TALL != 0) {
+      if (!v2) return set_error("16-row tile pass off the barrier-free sweep form", GADI_ERR_ARG);
+    }
     // tensor-map producer for the 3-D barrier-free passes (tmap.cuh): mode 1
     // boxes for two haloed inputs, mode 2 boxes for the epilogue inputs
     constexpr int TMM = TmaTm<P>::value ? 1 : (TmaTmEpi<P>::value ? 2 : 0);
@@ -211,6 +214,10 @@ inline int launch_sweep(Ctx* c, P& p, const HaloOut* hout = nullptr) {
     tm.ok = 0;
     if constexpr (TMM != 0) {
       if (v2 && c->tmap) tm.ok = tm_fill<P, TMM>(c, p, tm) ? 1 : 0;
+    }
+    if constexpr (P::TALL != 0) {
+      // its row-copy producer is not validated at 16 rows (scripts/tall_diag.py)
+      if (!tm.ok) return set_error("16-row tile pass without its tensor maps", GADI_ERR_ARG);
     }
     const size_t smem = v2 ? (tm.ok ? TmaShape2<P, TMM>::SMEM : TmaShape2<P>::SMEM) : TmaShape<P>::SMEM;
     const int NTH = v2 ? Tma2Threads<P>::value : TmaThreads<P>::NTOT;
@@ -261,6 +268,7 @@ inline int launch_sweep(Ctx* c, P& p, const HaloOut* hout = nullptr) {
     prof_end(c);
   } else {
     if constexpr (HasSide<P>::value) return set_error("z-lag pass off the TMA sweep path", GADI_ERR_ARG);
+    if constexpr (P::TALL != 0) return set_error("16-row tile pass off the TMA sweep path", GADI_ERR_ARG);
     p.g = make_geom(c, S::TZ, S::TY, P::VZ);
     const int nb = geom_blocks(p.g);
     if (nb > c->pstride) return set_error("sweep grid exceeds partials buffer", GADI_ERR_ARG);
@@ -546,11 +554,16 @@ struct Engine {
     GADI_TRY(launch_pw(c, hi));
     GADI_TRY(halo(c, c->R, sizeof(ST)));
     // z-lag (passes.cuh HcgA): only where every H-CG pass runs the barrier-free form
+    // HcgA on 16-row tiles (passes.cuh GeoT TALL) where it gets the tensor-map producer
+    typedef GeoT<ST, DIM, ZS, 1> GT;
+    const bool tall = DIM == 3 && c->tall && c->tmap && c->tma2 != 0 && tma_aligned<HcgA<GT>>(c) &&
+                      ((long long)c->ny * c->nz) % 16 == 0;  // tm_fill's plane-stride condition
     if (zlag_ok<HcgA<G, false, RF, true>>(c) && zlag_ok<HcgB<G, RF, true>>(c))
-      return h_loop_t<G, RF, true>(c, maxit);
-    return h_loop_t<G, RF, false>(c, maxit);
+      return tall ? h_loop_t<G, GT, RF, true>(c, maxit) : h_loop_t<G, G, RF, true>(c, maxit);
+    return tall ? h_loop_t<G, GT, RF, false>(c, maxit) : h_loop_t<G, G, RF, false>(c, maxit);
   }
-  template <class G, bool RF, bool ZL>
+  // GA: the geometry of the HcgA passes (G or its 16-row TALL form)
+  template <class G, class GA, bool RF, bool ZL>
   static int h_loop_t(Ctx* c, int maxit) {
     const CoefT<CT> H = cast_coef<CT>(c->H);
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
@@ -558,7 +571,7 @@ struct Engine {
         HaloOut ho;
         bool hf = false;
         if (k == 0) {
-          HcgA<G, true, RF> a;
+          HcgA<GA, true, RF> a;
           a.st = c->hst;
           a.r = (const ST*)c->R;
           a.pin = P[0];
@@ -567,7 +580,7 @@ struct Engine {
           hf = halo_begin(c, P[1], sizeof(ST), ho);
           GADI_TRY(launch_sweep(c, a, &ho));
         } else {
-          HcgA<G, false, RF, ZL> a;
+          HcgA<GA, false, RF, ZL> a;
           a.st = c->hst;
           a.r = (const ST*)c->R;
           a.pin = P[k & 1];

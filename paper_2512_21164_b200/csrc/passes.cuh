@@ -42,13 +42,22 @@ template <> struct CTOf<double> { typedef double type; };
 #ifndef GADI_VZ2B
 #define GADI_VZ2B 8  // bf16 / fp16 elements per lane
 #endif
-template <class ST_, int DIM, int ZS_>
+// TALL_ = 1 (3-D, tensor-map producer only): 16-row tiles at one CTA per SM
+// (a 200 KB stage ring, ~110 registers): the issue-bound HcgA sheds its
+// register rematerialisation (205 -> 186 us at 512^3 bf16); the DRAM-bound
+// two-epilogue passes (HcgB, CgnrP2) lose at that shape (256 -> 380 us),
+// so only HcgA takes it (profiles/ab_tile16_r2.jsonl).
+#ifndef GADI_TALL_BY
+#define GADI_TALL_BY 16
+#endif
+template <class ST_, int DIM, int ZS_, int TALL_ = 0>
 struct GeoT {
   typedef ST_ ST;
   typedef typename CTOf<ST_>::type CT;
+  static constexpr int TALL = DIM == 3 ? TALL_ : 0;
   static constexpr int VZ = sizeof(ST_) == 8 ? GADI_VZ64 : (sizeof(ST_) == 4 ? GADI_VZ32 : GADI_VZ2B);
   static constexpr int BZ = DIM == 3 ? 32 : 64;
-  static constexpr int BY = DIM == 3 ? GADI_BY3 : 1;
+  static constexpr int BY = DIM == 3 ? (TALL ? GADI_TALL_BY : GADI_BY3) : 1;
   static constexpr int ZS = ZS_;
   static constexpr int NT = BZ * BY;
 // 3 CTAs per SM (register budget ~62, a 74 KB stage ring each) measured
@@ -57,7 +66,7 @@ struct GeoT {
 #ifndef GADI_TMA_MINB
 #define GADI_TMA_MINB 3
 #endif
-  static constexpr int MINB = GADI_TMA_MINB;  // CTAs per SM the TMA sweep is register-budgeted for
+  static constexpr int MINB = TALL ? 1 : GADI_TMA_MINB;  // CTAs per SM the TMA sweep is register-budgeted for
 };
 
 // Kernel ids for the live per-kernel timers (gadi_prof_*).

@@ -154,9 +154,12 @@ template <class P> struct TmaShape {
 #define GADI_TMA_BUDGET_KB 74  // smem per CTA for passes run 3 per SM
 #endif
 #ifndef GADI_TMA_BUDGET1_KB
-#define GADI_TMA_BUDGET1_KB 110  // passes budgeted for fewer CTAs per SM (MINB < 3)
+#define GADI_TMA_BUDGET1_KB 110  // passes budgeted for 2 CTAs per SM
 #endif
-  static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : GADI_TMA_BUDGET1_KB) * 1024;
+#ifndef GADI_TMA_BUDGET_TALL_KB
+#define GADI_TMA_BUDGET_TALL_KB 200  // one CTA per SM (GeoT TALL)
+#endif
+  static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : (P::MINB == 2 ? GADI_TMA_BUDGET1_KB : GADI_TMA_BUDGET_TALL_KB)) * 1024;
   static constexpr int NST_RAW = (BUDGET - FBYTES) / STAGE;
   // a power of two: the consumers index the ring with % and / NST
   static constexpr int NST = NST_RAW >= 8 ? 8 : (NST_RAW >= 4 ? 4 : 2);

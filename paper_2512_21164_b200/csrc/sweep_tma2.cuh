@@ -204,7 +204,7 @@ struct TmaShape2 : TmaShape<P> {
     if constexpr (TM) return sb + off_epi_tm(j) + r * TZ * P::epi_esz(j);
     else return sb + Base::off_epi(j) + r * Base::rb_epi(j);
   }
-  static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : GADI_TMA_BUDGET1_KB) * 1024;
+  static constexpr int BUDGET = (P::MINB >= 3 ? GADI_TMA_BUDGET_KB : (P::MINB == 2 ? GADI_TMA_BUDGET1_KB : GADI_TMA_BUDGET_TALL_KB)) * 1024;
   static constexpr int NST_RAW = BUDGET / STAGE;
   static constexpr int NST = NST_RAW < 2 ? 2 : (NST_RAW > 12 ? 12 : NST_RAW);
   static constexpr size_t SMEM = (size_t)NST * STAGE + 3 * NST * sizeof(uint64_t);
