@@ -72,11 +72,11 @@ inline bool tm_fill(Ctx* c, const P& p, TmapSet& tm) {
   using BX = TmBox<P, TmaShape<P>>;
   if (c->ndim != 3 || ((long long)c->ny * c->nz) % 16) return false;
   for (int j = 0; j < P::NIN; ++j) {
-    if (!p.in_active(j) || TM != 1) continue;
+    if (!p.in_active(j) || (TM != 1 && TM != 3)) continue;
     if ((uintptr_t)p.in_ptr(j) % 16 || !tm_map(c, p.in_ptr(j), P::in_esz(j), BX::BW(j), TS::TY + 2, &tm.in[j]))
       return false;
   }
-  for (int j = 0; j < P::NE && TM == 2; ++j)
+  for (int j = 0; j < P::NE && (TM == 2 || TM == 3); ++j)
     if ((uintptr_t)p.epi_ptr(j) % 16 || !tm_map(c, p.epi_ptr(j), P::epi_esz(j), TS::TZ, TS::TY, &tm.epi[j]))
       return false;
   return true;
@@ -209,7 +209,7 @@ inline int launch_sweep(Ctx* c, P& p, const HaloOut* hout = nullptr) {
     }
     // tensor-map producer for the 3-D barrier-free passes (tmap.cuh): mode 1
     // boxes for two haloed inputs, mode 2 boxes for the epilogue inputs
-    constexpr int TMM = TmaTm<P>::value ? 1 : (TmaTmEpi<P>::value ? 2 : 0);
+    constexpr int TMM = TmaTm<P>::value ? (TmaTmBoth<P>::value ? 3 : 1) : (TmaTmEpi<P>::value ? 2 : 0);
     TmapSet tm;
     tm.ok = 0;
     if constexpr (TMM != 0) {
@@ -562,9 +562,14 @@ struct Engine {
       return tall ? h_loop_t<G, GT, RF, true>(c, maxit) : h_loop_t<G, G, RF, true>(c, maxit);
     return tall ? h_loop_t<G, GT, RF, false>(c, maxit) : h_loop_t<G, G, RF, false>(c, maxit);
   }
-  // GA: the geometry of the HcgA passes (G or its 16-row TALL form)
+  // GA: the geometry of the HcgA passes (G or its 16-row TALL form);
+  // GADI_TALL_HCGB = 1 (experiment) runs HcgB on it too
+#ifndef GADI_TALL_HCGB
+#define GADI_TALL_HCGB 0
+#endif
   template <class G, class GA, bool RF, bool ZL>
   static int h_loop_t(Ctx* c, int maxit) {
+    using GB = typename std::conditional<GADI_TALL_HCGB != 0, GA, G>::type;
     const CoefT<CT> H = cast_coef<CT>(c->H);
     ST* P[2] = {(ST*)c->P[0], (ST*)c->P[1]};
     auto iter = [&](int k) -> int {
@@ -591,7 +596,7 @@ struct Engine {
           GADI_TRY(launch_sweep(c, a, &ho));
         }
         GADI_TRY(halo_end(c, P[(k + 1) & 1], sizeof(ST), hf));
-        HcgB<G, RF, ZL> b;
+        HcgB<GB, RF, ZL> b;
         b.st = c->hst;
         b.p = P[(k + 1) & 1];
         b.z = (ST*)c->Z;

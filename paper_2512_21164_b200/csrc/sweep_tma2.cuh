@@ -183,7 +183,7 @@ struct TmaShape2 : TmaShape<P> {
     return o;
   }
   static constexpr int off_epi_tm(int j) {
-    int o = TM == 1 ? off_in_tm(P::NIN) : r128(Base::off_in(P::NIN));
+    int o = (TM == 1 || TM == 3) ? off_in_tm(P::NIN) : r128(Base::off_in(P::NIN));
     for (int i = 0; i < j; ++i) o += r128(TY * TZ * P::epi_esz(i));
     return o;
   }
@@ -192,7 +192,7 @@ struct TmaShape2 : TmaShape<P> {
   static __device__ __forceinline__ unsigned char* in_row_ptr(unsigned char* stages, int st, int j, int r, int tz) {
     const int esz = P::in_esz(j), hz = Base::hz(esz);
     unsigned char* sb = stages + (size_t)st * STAGE;
-    if constexpr (TM == 1) {
+    if constexpr (TM == 1 || TM == 3) {
       const int k = (BX::NB(j) == 2 && tz >= 16) ? 1 : 0;
       return sb + in_box_off(j, k) + r * BX::BW(j) * esz + (hz - k * BX::BW(j)) * esz;
     } else {

@@ -64,6 +64,17 @@ struct TmaTmEpi {
       GADI_TM_EPIBOX && SweepShape<P>::BZ == 32 && SweepShape<P>::BY > 1 && !TmaTm<P>::value && P::NE > 0;
 };
 
+// GADI_TALL_EPIBOX = 1: a 16-row (TALL) pass with epilogue inputs loads
+// haloed inputs AND epilogue tiles as boxes (TM = 3): 2 * 16 epilogue row
+// copies per stage from one producer warp are the alternative
+#ifndef GADI_TALL_EPIBOX
+#define GADI_TALL_EPIBOX 1
+#endif
+template <class P>
+struct TmaTmBoth {
+  static constexpr bool value = GADI_TALL_EPIBOX && TmaTm<P>::value && P::TALL != 0 && P::NE > 0;
+};
+
 template <class P, class TS>
 struct TmBox {
   static constexpr int W(int j) { return TS::TZ + 2 * TS::hz(P::in_esz(j)); }
@@ -102,7 +113,10 @@ template <class P, class TS, int TM>
 __device__ __forceinline__ void produce_stages_tm(const P& p, const SweepGeom& g, unsigned char* stages,
                                                   uint64_t* full, uint64_t* empty, int lane, const TmapSet& tm) {
   constexpr int TZ = TS::TZ, TY = TS::TY, NIN = P::NIN, NE = P::NE, NST = TS::NST;
-  constexpr int NRC = TM == 1 ? NE * TY : NIN * (TY + 2);  // row copies per stage
+  // TM 1: haloed inputs as boxes, epilogue rows copied; 2: the reverse;
+  // 3: both as boxes (no row copies)
+  constexpr bool INB = TM == 1 || TM == 3, EPB = TM == 2 || TM == 3;
+  constexpr int NRC = TM == 1 ? NE * TY : (TM == 2 ? NIN * (TY + 2) : 0);  // row copies per stage
   using B = TmBox<P, TS>;
   SegIter it(g, gridDim.x, blockIdx.x);
   int tile, xa, xb;
@@ -135,7 +149,7 @@ __device__ __forceinline__ void produce_stages_tm(const P& p, const SweepGeom& g
           for (int j = 0; j < NIN; ++j) {
             if (!p.in_active(j)) continue;
             const int esz = P::in_esz(j), hz = TS::hz(esz);
-            if (TM == 1)
+            if (INB)
               bytes += (unsigned)((TY + 2) * B::W(j) * esz);
             else
               bytes += (unsigned)((yhi - ylo) * (min(zt0 + TZ + hz, g.nz) - max(zt0 - hz, 0)) * esz);
@@ -143,11 +157,11 @@ __device__ __forceinline__ void produce_stages_tm(const P& p, const SweepGeom& g
           if (ev) {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
-              bytes += (unsigned)((TM == 2 ? TY : nyv) * (TM == 2 ? TZ : min(zt0 + TZ, g.nz) - zt0) * P::epi_esz(j));
+              bytes += (unsigned)((EPB ? TY : nyv) * (EPB ? TZ : min(zt0 + TZ, g.nz) - zt0) * P::epi_esz(j));
           }
         }
         mbar_expect_tx(&full[st], bytes);
-        if (pv && TM == 1) {
+        if (pv && INB) {
 #pragma unroll
           for (int j = 0; j < NIN; ++j) {
             if (!p.in_active(j)) continue;
@@ -158,14 +172,14 @@ __device__ __forceinline__ void produce_stages_tm(const P& p, const SweepGeom& g
                           y0 - 1, xc, &full[st]);
           }
         }
-        if (ev && TM == 2) {
+        if (ev && EPB) {
 #pragma unroll
           for (int j = 0; j < NE; ++j) tma_load_3d(TS::epi_row_ptr(stages, st, j, 0), &tm.epi[j], zt0, y0, xc, &full[st]);
         }
       }
       __syncwarp();
       // row copies, one per lane
-      if (TM == 1 ? ev : pv) {
+      if (NRC > 0 && (TM == 1 ? ev : pv)) {
         for (int q = lane; q < NRC; q += 32) {
           if constexpr (TM == 1) {
             const int j = q / TY, yy = y0 + q % TY;
