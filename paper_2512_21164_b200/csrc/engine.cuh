@@ -96,6 +96,9 @@ inline bool tma_aligned(const Ctx* c) {
 // environment (GADI_ZLAG=1) when the pass runs on the barrier-free TMA form.
 // Measured at 512^3 bf16 (profiles/ab_zlag_r2.jsonl): HcgA 204 -> 278 us,
 // HcgB 256 -> 190 us, one H-CG iteration 460 -> 468 us -- off by default.
+#ifndef GADI_TALL_ROWCOPY_OK
+#define GADI_TALL_ROWCOPY_OK 0  // let 16-row passes use the row-copy producer (bitwise the boxes: scripts/tall_diag2.py)
+#endif
 template <class P>
 inline bool zlag_ok(const Ctx* c) {
   if (!c->zlag_on) return false;
@@ -215,8 +218,9 @@ inline int launch_sweep(Ctx* c, P& p, const HaloOut* hout = nullptr) {
     if constexpr (TMM != 0) {
       if (v2 && c->tmap) tm.ok = tm_fill<P, TMM>(c, p, tm) ? 1 : 0;
     }
-    if constexpr (P::TALL != 0) {
-      // its row-copy producer is not validated at 16 rows (scripts/tall_diag.py)
+    if constexpr (P::TALL != 0 && !GADI_TALL_ROWCOPY_OK) {
+      // 16-row passes are measured with their tensor maps only (the row-copy
+      // producer issues 2 x 18 copies per stage from one warp)
       if (!tm.ok) return set_error("16-row tile pass without its tensor maps", GADI_ERR_ARG);
     }
     const size_t smem = v2 ? (tm.ok ? TmaShape2<P, TMM>::SMEM : TmaShape2<P>::SMEM) : TmaShape<P>::SMEM;
@@ -556,7 +560,7 @@ struct Engine {
     // z-lag (passes.cuh HcgA): only where every H-CG pass runs the barrier-free form
     // HcgA on 16-row tiles (passes.cuh GeoT TALL) where it gets the tensor-map producer
     typedef GeoT<ST, DIM, ZS, 1> GT;
-    const bool tall = DIM == 3 && c->tall && c->tmap && c->tma2 != 0 && tma_aligned<HcgA<GT>>(c) &&
+    const bool tall = DIM == 3 && c->tall && (c->tmap || GADI_TALL_ROWCOPY_OK) && c->tma2 != 0 && tma_aligned<HcgA<GT>>(c) &&
                       ((long long)c->ny * c->nz) % 16 == 0;  // tm_fill's plane-stride condition
     if (zlag_ok<HcgA<G, false, RF, true>>(c) && zlag_ok<HcgB<G, RF, true>>(c))
       return tall ? h_loop_t<G, GT, RF, true>(c, maxit) : h_loop_t<G, G, RF, true>(c, maxit);
