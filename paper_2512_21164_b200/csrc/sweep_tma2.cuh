@@ -389,11 +389,11 @@ __global__ void __launch_bounds__(Tma2Threads<P>::value, P::MINB)
       // GADI_XUNROLL = 3 unrolls the plane loop by the depth of the register
       // queue (fprev / fcur / fnext), letting the compiler rename instead of
       // moving the queue every plane
-#if GADI_XUNROLL == 3
-#pragma unroll 3
-#elif GADI_XUNROLL == 2
-#pragma unroll 2
-#endif
+      // 16-row (TALL) passes unroll by 3 at any GADI_XUNROLL: with their
+      // register headroom the renaming pays (HcgA 196.5 -> 189.6 us); at 3
+      // CTAs per SM it does not (profiles/ab_xunroll_r2.jsonl)
+      constexpr int XU = P::TALL ? 3 : GADI_XUNROLL;
+#pragma unroll XU
       for (int x = xa; x < xb; ++x, gidx += g.plane) {
         const int s = ps.slot;  // stage slot of plane x
         pn.next();              // plane x+1
