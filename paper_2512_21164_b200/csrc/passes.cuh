@@ -50,6 +50,9 @@ template <> struct CTOf<double> { typedef double type; };
 #ifndef GADI_TALL_BY
 #define GADI_TALL_BY 16
 #endif
+#ifndef GADI_TALL_MINB
+#define GADI_TALL_MINB 1
+#endif
 template <class ST_, int DIM, int ZS_, int TALL_ = 0>
 struct GeoT {
   typedef ST_ ST;
@@ -66,7 +69,7 @@ struct GeoT {
 #ifndef GADI_TMA_MINB
 #define GADI_TMA_MINB 3
 #endif
-  static constexpr int MINB = TALL ? 1 : GADI_TMA_MINB;  // CTAs per SM the TMA sweep is register-budgeted for
+  static constexpr int MINB = TALL ? GADI_TALL_MINB : GADI_TMA_MINB;  // CTAs per SM the TMA sweep is register-budgeted for
 };
 
 // Kernel ids for the live per-kernel timers (gadi_prof_*).
