@@ -753,7 +753,20 @@ struct Engine {
   // ------------------------------------------------------------ outer pass
   template <int DIM, int ZS, int UR, bool HAS_E, bool CPLX>
   static int outer_t(Ctx* c, double scale) {
-    typedef GeoT<double, DIM, ZS> G;
+    // GADI_TALL_OUTER = 1 (experiment): the outer pass on 16-row tiles
+#ifndef GADI_TALL_OUTER
+#define GADI_TALL_OUTER 0
+#endif
+    if constexpr (GADI_TALL_OUTER && DIM == 3) {
+      typedef GeoT<double, DIM, ZS, 1> GT;
+      if (c->tall && c->tmap && c->tma2 != 0 && tma_aligned<Outer<GT, ST, UR, HAS_E, CPLX>>(c) &&
+          ((long long)c->ny * c->nz) % 16 == 0)
+        return outer_g<GT, UR, HAS_E, CPLX>(c, scale);
+    }
+    return outer_g<GeoT<double, DIM, ZS>, UR, HAS_E, CPLX>(c, scale);
+  }
+  template <class G, int UR, bool HAS_E, bool CPLX>
+  static int outer_g(Ctx* c, double scale) {
     Outer<G, ST, UR, HAS_E, CPLX> o;
     o.x = c->x[c->xcur];
     o.y = (const ST*)c->Y;

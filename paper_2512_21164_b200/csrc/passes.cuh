@@ -814,7 +814,7 @@ struct Outer : G, PassBase {
   // two fp64 fields: 134 registers at 1 CTA/SM; GADI_OUTER_MINB = 2
   // (default) caps them at 102 for two CTAs per SM -- 64 bytes of spills,
   // but 1982 -> 1510 us at 512^3 (profiles/exp_om2.json)
-  static constexpr int MINB = GADI_OUTER_MINB;
+  static constexpr int MINB = G::TALL ? GADI_TALL_MINB : GADI_OUTER_MINB;
   static constexpr bool HAS_RED = true, ORD = true, TMA_OK = true;  // crd: v via load_epi_v
   // the barrier-free consumer form with tensor-map boxes for the haloed x and
   // y (GADI_OUTER_TMA2 = 1, default): 2867 -> 1997 us at 512^3 against the
